@@ -1,0 +1,234 @@
+// Small kernels around the decode/prefill chain: embedding gather, row
+// RMSNorm (prefill prologue), last-position gather, greedy argmax with the
+// device length register update, and the synthetic-weight generator.
+#include <math_constants.h>
+
+#include "common.cuh"
+#include "kernels.h"
+
+namespace fsvd::k {
+namespace {
+
+using namespace fsvd::dev;
+
+template <typename T>
+__global__ void embed_kernel(const T* emb, int ld, const int* tokens, int d, float* x, int x_ld) {
+    pdl_launch_dependents();
+    pdl_wait();
+    const int b = blockIdx.y;
+    const T* row = emb + static_cast<long long>(tokens[b]) * ld;
+    for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < d; i += gridDim.x * blockDim.x)
+        x[static_cast<long long>(b) * x_ld + i] = to_f32<T>(row[i]);
+}
+
+// reference rmsnorm (kernels_scalar.cpp:55-61): y = x * (1/sqrt(sum(x^2)/n + eps)) * gamma
+template <typename T>
+__global__ void rmsnorm_rows_kernel(const float* x, int x_ld, const float* gamma, float eps, int d, T* y, int y_ld) {
+    __shared__ float red[32];
+    __shared__ float inv;
+    const float* xr = x + static_cast<long long>(blockIdx.x) * x_ld;
+    float ss = 0.f;
+    for (int i = threadIdx.x; i < d; i += blockDim.x) ss = fmaf(xr[i], xr[i], ss);
+    ss = warp_sum(ss);
+    if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = ss;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        float t = 0.f;
+        for (int w = 0; w < static_cast<int>(blockDim.x >> 5); ++w) t += red[w];
+        inv = 1.0f / sqrtf(t / static_cast<float>(d) + eps);
+    }
+    __syncthreads();
+    T* yr = y + static_cast<long long>(blockIdx.x) * y_ld;
+    for (int i = threadIdx.x; i < d; i += blockDim.x) yr[i] = from_f32<T>(xr[i] * inv * gamma[i]);
+}
+
+__global__ void gather_last_kernel(const float* x, int x_ld, int T, int d, float* xl, int xl_ld) {
+    const int b = blockIdx.y;
+    const float* src = x + (static_cast<long long>(b) * T + T - 1) * x_ld;
+    for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < d; i += gridDim.x * blockDim.x)
+        xl[static_cast<long long>(b) * xl_ld + i] = src[i];
+}
+
+__device__ __forceinline__ bool better(float v, int i, float bv, int bi) {
+    return v > bv || (v == bv && i < bi);
+}
+
+// One CTA per sequence; ties -> lowest index (reference math.hpp:132-140).
+// The last CTA to finish advances the length register and the step counter.
+__global__ void __launch_bounds__(1024) argmax_kernel(const float* logits, int vocab, int* tokens, int* pos,
+                                                      int pos_inc, int* out, int out_ld, int* step,
+                                                      unsigned* ticket) {
+    pdl_launch_dependents();
+    pdl_wait();
+    __shared__ float sv[32];
+    __shared__ int si[32];
+    __shared__ int last;
+    const int b = blockIdx.x;
+    const float* lr = logits + static_cast<long long>(b) * vocab;
+    float bv = -CUDART_INF_F;
+    int bi = 0x7fffffff;
+    for (int i = threadIdx.x; i < vocab; i += blockDim.x) {
+        const float v = lr[i];
+        if (better(v, i, bv, bi)) {
+            bv = v;
+            bi = i;
+        }
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+        const float ov = __shfl_xor_sync(0xffffffffu, bv, o);
+        const int oi = __shfl_xor_sync(0xffffffffu, bi, o);
+        if (better(ov, oi, bv, bi)) {
+            bv = ov;
+            bi = oi;
+        }
+    }
+    if ((threadIdx.x & 31) == 0) {
+        sv[threadIdx.x >> 5] = bv;
+        si[threadIdx.x >> 5] = bi;
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        for (int w = 1; w < static_cast<int>(blockDim.x >> 5); ++w)
+            if (better(sv[w], si[w], bv, bi)) {
+                bv = sv[w];
+                bi = si[w];
+            }
+        if (bi == 0x7fffffff) bi = 0;  // all-NaN row
+        tokens[b] = bi;
+        if (out) out[static_cast<long long>(b) * out_ld + *step] = bi;
+        __threadfence();
+        last = atomicAdd(ticket, 1u) == gridDim.x - 1;
+        if (last) {
+            *pos += pos_inc;
+            if (step) *step += 1;
+            *ticket = 0u;
+        }
+    }
+}
+
+__global__ void set_int_kernel(int* p, int v) { *p = v; }
+__global__ void add_int_kernel(int* p, int v) {
+    pdl_launch_dependents();
+    pdl_wait();
+    *p += v;
+}
+
+__device__ __forceinline__ float round_bf16_dev(float x) {
+    uint32_t u = __float_as_uint(x);
+    if ((u & 0x7F800000u) == 0x7F800000u) return x;
+    u += 0x7FFFu + ((u >> 16) & 1u);
+    return __uint_as_float(u & 0xFFFF0000u);
+}
+
+// include/fsvd/synth.hpp synth_value, bit for bit.
+__device__ __forceinline__ float synth_dev(uint64_t seed, uint64_t idx, double amp, int kind) {
+    uint64_t z = seed + (idx + 1) * 0x9E3779B97F4A7C15ull;
+    z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ull;
+    z = (z ^ (z >> 27)) * 0x94D049BB133111EBull;
+    z ^= z >> 31;
+    const double unit = __dmul_rn(static_cast<double>(z >> 11), 0x1.0p-53);
+    const double sym = __dsub_rn(__dmul_rn(2.0, unit), 1.0);
+    double v;
+    if (kind == 1)
+        v = __dadd_rn(1.0, __dmul_rn(sym, amp));
+    else if (kind == 2)
+        v = __dadd_rn(0.5, unit);
+    else
+        v = __dmul_rn(sym, amp);
+    return round_bf16_dev(__double2float_rn(v));
+}
+
+// Iteration order follows the destination (transposed targets walk r
+// fastest) so the writes coalesce; the values are a pure function of the
+// logical index, so the order does not change them.
+__global__ void synth_fill_kernel(const SynthFill f) {
+    const long long n = f.rows * f.cols;
+    const bool by_col = f.rs == 1 && f.cs != 1;
+    for (long long t = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; t < n;
+         t += static_cast<long long>(gridDim.x) * blockDim.x) {
+        long long r, c;
+        if (by_col) {
+            c = t / f.rows;
+            r = t - c * f.rows;
+        } else {
+            r = t / f.cols;
+            c = t - r * f.cols;
+        }
+        const long long i = r * f.cols + c;
+        float v = synth_dev(f.seed, f.offset + i, f.amp, f.kind);
+        if (f.fold == 1) {
+            const float s = synth_dev(f.seed, f.scale_offset + r, 0.0, 2);
+            v = __fmul_rn(v, __fdiv_rn(1.0f, s));
+        } else if (f.fold == 2) {
+            const float s = synth_dev(f.seed, f.scale_offset + c, 0.0, 2);
+            v = __fmul_rn(v, s);
+        }
+        const long long o = r * f.rs + c * f.cs;
+        if (f.dt == kBF16)
+            static_cast<__nv_bfloat16*>(f.dst)[o] = __float2bfloat16_rn(v);
+        else
+            static_cast<float*>(f.dst)[o] = v;
+    }
+}
+
+cudaLaunchConfig_t pdl_cfg(dim3 grid, dim3 block, cudaStream_t s, bool pdl, cudaLaunchAttribute* attr) {
+    cudaLaunchConfig_t cfg{};
+    cfg.gridDim = grid;
+    cfg.blockDim = block;
+    cfg.stream = s;
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = pdl ? 1 : 0;
+    return cfg;
+}
+
+}  // namespace
+
+void embed(WType wt, const void* emb, int ld_emb, const int* tokens, int n, int d, float* x, int x_ld,
+           cudaStream_t s, bool pdl) {
+    cudaLaunchAttribute attr[1];
+    auto cfg = pdl_cfg(dim3((d + 255) / 256 < 16 ? (d + 255) / 256 : 16, n), dim3(256), s, pdl, attr);
+    if (wt == kBF16)
+        cudaLaunchKernelEx(&cfg, embed_kernel<__nv_bfloat16>, static_cast<const __nv_bfloat16*>(emb), ld_emb,
+                           tokens, d, x, x_ld);
+    else
+        cudaLaunchKernelEx(&cfg, embed_kernel<float>, static_cast<const float*>(emb), ld_emb, tokens, d, x, x_ld);
+}
+
+void rmsnorm_rows(WType wt, const float* x, int x_ld, const float* gamma, float eps, int rows, int d, void* y,
+                  int y_ld, cudaStream_t s) {
+    if (wt == kBF16)
+        rmsnorm_rows_kernel<__nv_bfloat16><<<rows, 256, 0, s>>>(x, x_ld, gamma, eps, d,
+                                                                  static_cast<__nv_bfloat16*>(y), y_ld);
+    else
+        rmsnorm_rows_kernel<float><<<rows, 256, 0, s>>>(x, x_ld, gamma, eps, d, static_cast<float*>(y), y_ld);
+}
+
+void gather_last(const float* x, int x_ld, int batch, int T, int d, float* xl, int xl_ld, cudaStream_t s) {
+    gather_last_kernel<<<dim3(4, batch), 256, 0, s>>>(x, x_ld, T, d, xl, xl_ld);
+}
+
+void argmax_step(const float* logits, int batch, int vocab, int* tokens, int* pos, int pos_inc, int* out,
+                      int out_ld, int* step, unsigned* ticket, cudaStream_t s, bool pdl) {
+    cudaLaunchAttribute attr[1];
+    auto cfg = pdl_cfg(dim3(batch), dim3(1024), s, pdl, attr);
+    cudaLaunchKernelEx(&cfg, argmax_kernel, logits, vocab, tokens, pos, pos_inc, out, out_ld, step, ticket);
+}
+
+void set_int(int* p, int v, cudaStream_t s) { set_int_kernel<<<1, 1, 0, s>>>(p, v); }
+void add_int(int* p, int v, cudaStream_t s, bool pdl) {
+    cudaLaunchAttribute attr[1];
+    auto cfg = pdl_cfg(dim3(1), dim3(1), s, pdl, attr);
+    cudaLaunchKernelEx(&cfg, add_int_kernel, p, v);
+}
+
+void synth_fill(const SynthFill& f, cudaStream_t s) {
+    const long long n = f.rows * f.cols;
+    long long blocks = (n + 255) / 256;
+    if (blocks > 148 * 32) blocks = 148 * 32;
+    synth_fill_kernel<<<static_cast<unsigned>(blocks), 256, 0, s>>>(f);
+}
+
+}  // namespace fsvd::k

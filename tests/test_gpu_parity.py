@@ -1,0 +1,196 @@
+"""GPU parity: the CUDA path through the C ABI vs the CPU oracle.
+
+North-star tolerances (BASELINE.json): max relative logit error <= 1e-4 in
+the fp32 mode and <= 2e-2 in bf16, error = max_rows max|d| / max|ref|
+(SURVEY.md §8c). Oracle = f64 restatement (oracle/fsvd_oracle.cpp) on the
+same normalize<float> weights and tokens. Greedy-token agreement is reported,
+not required.
+"""
+import numpy as np
+import pytest
+
+pytestmark = pytest.mark.gpu
+
+TOL = {"f32": 1e-4, "bf16": 2e-2}
+
+
+def _spec(fsvd, family="A", cfg=None, seed=5, conditioned=True, rho=0.5, jitter=0.0, cap=512):
+    cfg = cfg or fsvd.ModelConfig(2, 128, 4, 32, 256, 512)
+    return fsvd.SynthSpec(cfg, capacity=cap, family=family, rho=rho, group_size=2, seed=seed,
+                          conditioned=conditioned, rank_jitter=jitter)
+
+
+def _prompt(cfg, T, seed=2, batch=1):
+    rng = np.random.default_rng(seed)
+    return rng.integers(0, cfg.vocab, size=(batch, T), dtype=np.int32)
+
+
+@pytest.mark.parametrize("dtype", ["f32", "bf16"])
+@pytest.mark.parametrize("family", ["A", "B", "C", "D"])
+def test_prefill_decode_vs_oracle(fsvd, oracle_mod, dtype, family):
+    spec = _spec(fsvd, family, jitter=0.3 if family in "BD" else 0.0)
+    cfg = spec.config
+    prompt = _prompt(cfg, 37)
+    om = oracle_mod.OracleModel.synthetic(spec)
+    osess = om.session(f64=True, ffn="no_merge", capacity=512)
+    want = [osess.prefill(prompt[0])]
+    toks = [int(np.argmax(want[0]))]
+    for _ in range(6):
+        want.append(osess.decode_step(toks[-1]))
+        toks.append(int(np.argmax(want[-1])))
+
+    model = fsvd.Model.synthetic(spec, dtype=dtype)
+    for plan in ("eager", "per_layer", "full_step"):
+        s = fsvd.Session(model, batch=1, capacity=512, plan=plan)
+        got = [s.prefill(prompt)[0]]
+        for t in toks[:-1]:
+            got.append(s.decode_step([t])[0])
+        errs = [oracle_mod.rel_err(g, w) for g, w in zip(got, want)]
+        assert max(errs) <= TOL[dtype], (plan, errs)
+        assert s.position == 37 + 6
+
+
+@pytest.mark.parametrize("dtype", ["f32", "bf16"])
+def test_device_synthetic_matches_host_upload(fsvd, dtype):
+    """fsvd_model_synthetic (device generator) == normalize<float> upload, bitwise."""
+    for family in "ABCD":
+        spec = _spec(fsvd, family, jitter=0.3)
+        cfg = spec.config
+        can = fsvd.Canonical.synthetic(spec)
+        m_dev = fsvd.Model.synthetic(spec, dtype=dtype)
+        m_host = fsvd.Model.from_canonical(can, dtype=dtype)
+        for layer in range(cfg.n_layers):
+            for p in fsvd.PROJ:
+                r = can.rank(layer, p)
+                din = cfg.d_ff if p == "down" else cfg.d_model
+                dout = cfg.d_ff if p in ("up", "gate") else cfg.d_model
+                for which, shape in (("A", (din, r)), ("B", (r, dout))):
+                    a = m_dev.factor(layer, p, which, shape)
+                    b = m_host.factor(layer, p, which, shape)
+                    assert np.array_equal(a.view(np.uint32), b.view(np.uint32)), (family, layer, p, which)
+                    if dtype == "f32":
+                        c = can.tensor(f"layers.{layer}.{p}.{which}", shape)
+                        assert np.array_equal(a.view(np.uint32), c.view(np.uint32))
+
+
+def test_packed_equals_no_merge_bitwise(fsvd):
+    """SPEC.md:547 / :261: packed FFN == no_merge bitwise (per-row fixed reduction order)."""
+    spec = _spec(fsvd, "A")
+    prompt = _prompt(spec.config, 20)
+    model = fsvd.Model.synthetic(spec, dtype="bf16")
+    outs = {}
+    for ffn in ("no_merge", "packed"):
+        s = fsvd.Session(model, batch=1, capacity=512, ffn=ffn, plan="eager")
+        lg = [s.prefill(prompt)[0]]
+        for t in range(5):
+            lg.append(s.decode_step([int(np.argmax(lg[-1]))])[0])
+        outs[ffn] = np.stack(lg)
+    assert np.array_equal(outs["packed"][1:].view(np.uint32), outs["no_merge"][1:].view(np.uint32))
+
+
+def test_replay_equals_eager_bitwise(fsvd):
+    """plan replay == eager, bitwise, same backend."""
+    spec = _spec(fsvd, "C")
+    prompt = _prompt(spec.config, 25)
+    model = fsvd.Model.synthetic(spec, dtype="bf16")
+    outs = {}
+    for plan in ("eager", "per_layer", "full_step"):
+        s = fsvd.Session(model, batch=1, capacity=512, ffn="packed", plan=plan)
+        lg = [s.prefill(prompt)[0]]
+        for _ in range(8):
+            lg.append(s.decode_step([int(np.argmax(lg[-1]))])[0])
+        outs[plan] = np.stack(lg)
+    assert np.array_equal(outs["per_layer"].view(np.uint32), outs["eager"].view(np.uint32))
+    assert np.array_equal(outs["full_step"].view(np.uint32), outs["eager"].view(np.uint32))
+
+
+def test_generate_matches_stepwise(fsvd, oracle_mod):
+    spec = _spec(fsvd, "A")
+    prompt = _prompt(spec.config, 12)
+    model = fsvd.Model.synthetic(spec, dtype="f32")
+    s = fsvd.Session(model, batch=1, capacity=512, plan="full_step")
+    toks = s.generate(prompt, 10)[0]
+    assert s.position == 12 + 9
+    om = oracle_mod.OracleModel.synthetic(spec)
+    want = om.session(f64=True, capacity=512).generate(prompt[0], 10)
+    agree = float(np.mean(toks == want))
+    assert toks[0] == want[0]  # first token always agrees in fp32 (margin >> 1e-4)
+    assert agree >= 0.5, (toks, want)
+
+
+def test_batch_sequences_independent(fsvd, oracle_mod):
+    spec = _spec(fsvd, "A")
+    cfg = spec.config
+    prompt = _prompt(cfg, 19, batch=3)
+    om = oracle_mod.OracleModel.synthetic(spec)
+    model = fsvd.Model.synthetic(spec, dtype="f32")
+    s = fsvd.Session(model, batch=3, capacity=512, plan="per_layer")
+    lp = s.prefill(prompt)
+    nxt = np.argmax(lp, axis=1).astype(np.int32)
+    ld = s.decode_step(nxt)
+    for b in range(3):
+        os_ = om.session(f64=True, capacity=512)
+        assert oracle_mod.rel_err(lp[b], os_.prefill(prompt[b])) <= 1e-4
+        assert oracle_mod.rel_err(ld[b], os_.decode_step(int(nxt[b]))) <= 1e-4
+
+
+def test_kv_cache_matches_oracle(fsvd, oracle_mod):
+    """SPEC.md:361 cache consistency: cached K/V rows equal the oracle's."""
+    spec = _spec(fsvd, "B", jitter=0.2)
+    prompt = _prompt(spec.config, 30)
+    om = oracle_mod.OracleModel.synthetic(spec)
+    osess = om.session(f64=True, capacity=512)
+    osess.prefill(prompt[0])
+    osess.decode_step(3)
+    s = fsvd.Session(fsvd.Model.synthetic(spec, dtype="f32"), batch=1, capacity=512)
+    s.prefill(prompt)
+    s.decode_step([3])
+    for layer in (0, 1):
+        for which in "KV":
+            got = s.read_kv(layer, 0, which, 0, 31)
+            want = osess.read_kv(layer, which, 0, 31)
+            assert np.abs(got - want).max() <= 1e-4 * np.abs(want).max()
+
+
+def test_chunked_prompt_and_capacity_errors(fsvd, oracle_mod):
+    spec = _spec(fsvd, "A", cap=64)
+    prompt = _prompt(spec.config, 60)
+    model = fsvd.Model.synthetic(spec, dtype="f32")
+    s = fsvd.Session(model, batch=1, capacity=64)
+    with pytest.raises(fsvd.CapacityError):
+        s.prefill(_prompt(spec.config, 65))
+    with pytest.raises(fsvd.ShapeError):
+        s.prefill(np.zeros((1, 0), np.int32))
+    with pytest.raises(fsvd.ShapeError):
+        s.decode_step([1])  # before prefill
+    lp = s.prefill(prompt)
+    om = oracle_mod.OracleModel.synthetic(spec)
+    assert oracle_mod.rel_err(lp[0], om.session(f64=True, capacity=64).prefill(prompt[0])) <= 1e-4
+    for t in range(4):
+        s.decode_step([t])
+    with pytest.raises(fsvd.CapacityError):
+        s.decode_step([1])
+    s.reset()
+    assert s.position == 0
+
+
+def test_dispatch_counts(fsvd):
+    """dispatches per step full_step < per_layer < eager."""
+    spec = _spec(fsvd, "A")
+    model = fsvd.Model.synthetic(spec, dtype="bf16")
+    counts = {}
+    for plan in ("eager", "per_layer", "full_step"):
+        s = fsvd.Session(model, batch=1, capacity=512, plan=plan)
+        s.prefill(_prompt(spec.config, 8))
+        s.decode_step([1])
+        s.decode_step([2])
+        counts[plan] = s.stats().last_dispatches
+        if plan != "eager":
+            assert s.resolved()[0] == "packed"
+        else:
+            assert s.resolved()[0] == "no_merge"
+    L = spec.config.n_layers
+    assert counts["per_layer"] == L + 3
+    assert counts["full_step"] == 1
+    assert counts["eager"] >= 5 * counts["full_step"]
+    assert counts["full_step"] < counts["per_layer"] < counts["eager"]
