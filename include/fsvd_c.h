@@ -154,6 +154,15 @@ fsvd_status fsvd_session_position(const fsvd_session* s, uint64_t* position);
 fsvd_status fsvd_session_reset(fsvd_session* s);
 fsvd_status fsvd_session_stats(const fsvd_session* s, fsvd_step_stats* st);
 fsvd_status fsvd_session_resolved(const fsvd_session* s, fsvd_ffn_backend* ffn, fsvd_plan_mode* plan);
+/* Decode engine: megakernel = 1 when the persistent decode megakernel runs the
+ * step (else one kernel per op); ring stage bytes / stage count / attention
+ * splits of the megakernel. */
+fsvd_status fsvd_session_engine(const fsvd_session* s, int32_t* megakernel, int32_t* stage_bytes, int32_t* nstage,
+                                int32_t* attn_splits);
+/* Profiling (FSVD_TRACE=1 at session creation): per-CTA per-phase
+ * %globaltimer stamps of the last full-step megakernel launch,
+ * out = [grid][phases][4] (wait start, barrier passed, input staged, done). */
+fsvd_status fsvd_session_trace(fsvd_session* s, uint64_t* out, uint64_t count, int32_t* phases, int32_t* grid);
 /* Read cached K (which=0) or V (which=1) rows [pos0, pos0+npos) of sequence b
  * at layer l as f32, [npos][d_model] (head-major within a row, like the dense
  * reference K = rmsnorm(x)·W_k). */

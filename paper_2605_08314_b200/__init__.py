@@ -201,6 +201,8 @@ def lib() -> C.CDLL:
         "fsvd_session_stats": ([vp, C.POINTER(_Stats)], C.c_int),
         "fsvd_session_resolved": ([vp, C.POINTER(C.c_int), C.POINTER(C.c_int)], C.c_int),
         "fsvd_session_read_kv": ([vp, u64, u64, i32, u64, u64, f32p], C.c_int),
+        "fsvd_session_engine": ([vp, i32p, i32p, i32p, i32p], C.c_int),
+        "fsvd_session_trace": ([vp, C.POINTER(u64), u64, i32p, i32p], C.c_int),
         "fsvd_session_destroy": ([vp], C.c_int),
     }
     for name, (args, res) in sig.items():
@@ -220,7 +222,7 @@ def exported_symbols() -> list[str]:
             "fsvd_session_create", "fsvd_prefill", "fsvd_decode_step", "fsvd_generate", "fsvd_prefill_device",
             "fsvd_decode_step_device", "fsvd_generate_device", "fsvd_session_sync", "fsvd_session_stream",
             "fsvd_session_position", "fsvd_session_reset", "fsvd_session_stats", "fsvd_session_resolved",
-            "fsvd_session_read_kv", "fsvd_session_destroy"]
+            "fsvd_session_read_kv", "fsvd_session_engine", "fsvd_session_trace", "fsvd_session_destroy"]
 
 
 def _check(status: int) -> None:
@@ -448,6 +450,20 @@ class Session:
         f, p = C.c_int(), C.c_int()
         _check(lib().fsvd_session_resolved(self._h, C.byref(f), C.byref(p)))
         return FFN_NAMES[f.value], PLAN_NAMES[p.value]
+
+    def engine(self) -> dict:
+        v = [C.c_int32() for _ in range(4)]
+        _check(lib().fsvd_session_engine(self._h, *[C.byref(x) for x in v]))
+        return {"megakernel": bool(v[0].value), "unit_bytes": v[1].value, "warps_per_cta": v[2].value,
+                "attn_splits": v[3].value}
+
+    def trace(self, max_phases: int = 4096) -> np.ndarray:
+        """[grid, phases, 8] ns stamps of the last traced full step (FSVD_TRACE=1)."""
+        buf = np.zeros(148 * 2 * max_phases * 8, dtype=np.uint64)
+        ph, g = C.c_int32(), C.c_int32()
+        _check(lib().fsvd_session_trace(self._h, buf.ctypes.data_as(C.POINTER(C.c_uint64)), buf.size,
+                                        C.byref(ph), C.byref(g)))
+        return buf[: g.value * ph.value * 8].reshape(g.value, ph.value, 8)
 
     def read_kv(self, layer: int, b: int, which: str, pos0: int, npos: int) -> np.ndarray:
         out = np.empty((npos, self._cfg.d_model), dtype=np.float32)

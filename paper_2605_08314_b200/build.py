@@ -46,7 +46,7 @@ def json_include_dir() -> Path:
 
 HOST_SOURCES = ["host/model.cpp", "host/checkpoint.cpp", "host/canonical.cpp", "host/synth.cpp", "capi/capi.cpp"]
 CUDA_SOURCES = [
-    "cuda/gemv.cu",
+    "cuda/decode_mk.cu",
     "cuda/attention.cu",
     "cuda/gemm_simt.cu",
     "cuda/gemm.cu",

@@ -454,6 +454,29 @@ fsvd_status fsvd_session_resolved(const fsvd_session* s, fsvd_ffn_backend* ffn, 
     });
 }
 
+fsvd_status fsvd_session_engine(const fsvd_session* s, int32_t* megakernel, int32_t* stage_bytes, int32_t* nstage,
+                                int32_t* attn_splits) {
+    return guarded([&] {
+        need(s, "session");
+        const auto e = s->s->engine();
+        if (megakernel) *megakernel = e[0];
+        if (stage_bytes) *stage_bytes = e[1];
+        if (nstage) *nstage = e[2];
+        if (attn_splits) *attn_splits = e[3];
+    });
+}
+
+fsvd_status fsvd_session_trace(fsvd_session* s, uint64_t* out, uint64_t count, int32_t* phases, int32_t* grid) {
+    return guarded([&] {
+        need(s, "session");
+        need(out, "out");
+        int g = 0;
+        const int n = s->s->read_trace(reinterpret_cast<unsigned long long*>(out), count, &g);
+        if (phases) *phases = n;
+        if (grid) *grid = g;
+    });
+}
+
 fsvd_status fsvd_session_read_kv(fsvd_session* s, uint64_t layer, uint64_t b, int32_t which, uint64_t pos0,
                                  uint64_t npos, float* out) {
     return guarded([&] {

@@ -2,7 +2,8 @@
 //
 // Used for the fp32 parity mode (f32 runtime accumulates in
 // f32), where tensor cores would change the arithmetic. The bf16 mode runs
-// the tcgen05 GEMM in gemm_tc.cu. Same epilogues as the tensor-core path:
+// the tcgen05 GEMM in gemm_tc.cu. Weights are read from the tile layout
+// (layout.h). Same epilogues as the tensor-core path:
 // plain store, residual add, RoPE + KV append for the QKV reconstruction
 // (SPEC.md:308), and the dual up/gate SiLU.mul.
 #include "common.cuh"
@@ -43,7 +44,8 @@ __global__ void __launch_bounds__(NT) gemm_simt_kernel(const __grid_constant__ G
 #pragma unroll
     for (int d = 0; d < (DUAL ? 2 : 1); ++d) {
         const GemvSeg& sd = a.seg[DUAL ? d : s];
-        const T* Wt = static_cast<const T*>(sd.w);
+        const char* Wt = static_cast<const char*>(sd.w);
+        const WLayout lay = sd.layout(sizeof(T));
         for (int k0 = 0; k0 < sd.k; k0 += BK) {
             __syncthreads();
             for (int i = tid; i < BM * BK; i += NT) {
@@ -54,7 +56,7 @@ __global__ void __launch_bounds__(NT) gemm_simt_kernel(const __grid_constant__ G
             for (int i = tid; i < BN * BK; i += NT) {
                 const int n = i / BK, kk = i % BK;
                 const int r = n0 + n, k = k0 + kk;
-                Ws[0][kk][n] = (r < sd.rows && k < sd.k) ? to_f32<T>(Wt[static_cast<long long>(r) * sd.ldw + k]) : 0.f;
+                Ws[0][kk][n] = (r < sd.rows && k < sd.k) ? to_f32<T>(*reinterpret_cast<const T*>(Wt + lay.offset(r, k))) : 0.f;
             }
             __syncthreads();
 #pragma unroll 8

@@ -1,8 +1,6 @@
-// Small kernels around the decode/prefill chain: embedding gather, row
-// RMSNorm (prefill prologue), last-position gather, greedy argmax with the
-// device length register update, and the synthetic-weight generator.
-#include <math_constants.h>
-
+// Small kernels around the prefill chain and model setup: embedding gather,
+// row RMSNorm (prefill prologue), last-position gather, the length-register
+// setter and the synthetic-weight generator.
 #include "common.cuh"
 #include "kernels.h"
 
@@ -13,8 +11,6 @@ using namespace fsvd::dev;
 
 template <typename T>
 __global__ void embed_kernel(const T* emb, int ld, const int* tokens, int d, float* x, int x_ld) {
-    pdl_launch_dependents();
-    pdl_wait();
     const int b = blockIdx.y;
     const T* row = emb + static_cast<long long>(tokens[b]) * ld;
     for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < d; i += gridDim.x * blockDim.x)
@@ -49,70 +45,7 @@ __global__ void gather_last_kernel(const float* x, int x_ld, int T, int d, float
         xl[static_cast<long long>(b) * xl_ld + i] = src[i];
 }
 
-__device__ __forceinline__ bool better(float v, int i, float bv, int bi) {
-    return v > bv || (v == bv && i < bi);
-}
-
-// One CTA per sequence; ties -> lowest index (reference math.hpp:132-140).
-// The last CTA to finish advances the length register and the step counter.
-__global__ void __launch_bounds__(1024) argmax_kernel(const float* logits, int vocab, int* tokens, int* pos,
-                                                      int pos_inc, int* out, int out_ld, int* step,
-                                                      unsigned* ticket) {
-    pdl_launch_dependents();
-    pdl_wait();
-    __shared__ float sv[32];
-    __shared__ int si[32];
-    __shared__ int last;
-    const int b = blockIdx.x;
-    const float* lr = logits + static_cast<long long>(b) * vocab;
-    float bv = -CUDART_INF_F;
-    int bi = 0x7fffffff;
-    for (int i = threadIdx.x; i < vocab; i += blockDim.x) {
-        const float v = lr[i];
-        if (better(v, i, bv, bi)) {
-            bv = v;
-            bi = i;
-        }
-    }
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) {
-        const float ov = __shfl_xor_sync(0xffffffffu, bv, o);
-        const int oi = __shfl_xor_sync(0xffffffffu, bi, o);
-        if (better(ov, oi, bv, bi)) {
-            bv = ov;
-            bi = oi;
-        }
-    }
-    if ((threadIdx.x & 31) == 0) {
-        sv[threadIdx.x >> 5] = bv;
-        si[threadIdx.x >> 5] = bi;
-    }
-    __syncthreads();
-    if (threadIdx.x == 0) {
-        for (int w = 1; w < static_cast<int>(blockDim.x >> 5); ++w)
-            if (better(sv[w], si[w], bv, bi)) {
-                bv = sv[w];
-                bi = si[w];
-            }
-        if (bi == 0x7fffffff) bi = 0;  // all-NaN row
-        tokens[b] = bi;
-        if (out) out[static_cast<long long>(b) * out_ld + *step] = bi;
-        __threadfence();
-        last = atomicAdd(ticket, 1u) == gridDim.x - 1;
-        if (last) {
-            *pos += pos_inc;
-            if (step) *step += 1;
-            *ticket = 0u;
-        }
-    }
-}
-
 __global__ void set_int_kernel(int* p, int v) { *p = v; }
-__global__ void add_int_kernel(int* p, int v) {
-    pdl_launch_dependents();
-    pdl_wait();
-    *p += v;
-}
 
 __device__ __forceinline__ float round_bf16_dev(float x) {
     uint32_t u = __float_as_uint(x);
@@ -144,7 +77,7 @@ __device__ __forceinline__ float synth_dev(uint64_t seed, uint64_t idx, double a
 // logical index, so the order does not change them.
 __global__ void synth_fill_kernel(const SynthFill f) {
     const long long n = f.rows * f.cols;
-    const bool by_col = f.rs == 1 && f.cs != 1;
+    const bool by_col = f.mode == 1 || (f.rs == 1 && f.cs != 1);
     for (long long t = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; t < n;
          t += static_cast<long long>(gridDim.x) * blockDim.x) {
         long long r, c;
@@ -164,37 +97,32 @@ __global__ void synth_fill_kernel(const SynthFill f) {
             const float s = synth_dev(f.seed, f.scale_offset + c, 0.0, 2);
             v = __fmul_rn(v, s);
         }
-        const long long o = r * f.rs + c * f.cs;
-        if (f.dt == kBF16)
-            static_cast<__nv_bfloat16*>(f.dst)[o] = __float2bfloat16_rn(v);
-        else
-            static_cast<float*>(f.dst)[o] = v;
+        if (f.mode == 1) {
+            char* p = static_cast<char*>(f.dst) + f.lay.offset(static_cast<int>(c), static_cast<int>(r));
+            if (f.dt == kBF16)
+                *reinterpret_cast<__nv_bfloat16*>(p) = __float2bfloat16_rn(v);
+            else
+                *reinterpret_cast<float*>(p) = v;
+        } else {
+            const long long o = r * f.rs + c * f.cs;
+            if (f.dt == kBF16)
+                static_cast<__nv_bfloat16*>(f.dst)[o] = __float2bfloat16_rn(v);
+            else
+                static_cast<float*>(f.dst)[o] = v;
+        }
     }
-}
-
-cudaLaunchConfig_t pdl_cfg(dim3 grid, dim3 block, cudaStream_t s, bool pdl, cudaLaunchAttribute* attr) {
-    cudaLaunchConfig_t cfg{};
-    cfg.gridDim = grid;
-    cfg.blockDim = block;
-    cfg.stream = s;
-    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
-    attr[0].val.programmaticStreamSerializationAllowed = 1;
-    cfg.attrs = attr;
-    cfg.numAttrs = pdl ? 1 : 0;
-    return cfg;
 }
 
 }  // namespace
 
 void embed(WType wt, const void* emb, int ld_emb, const int* tokens, int n, int d, float* x, int x_ld,
-           cudaStream_t s, bool pdl) {
-    cudaLaunchAttribute attr[1];
-    auto cfg = pdl_cfg(dim3((d + 255) / 256 < 16 ? (d + 255) / 256 : 16, n), dim3(256), s, pdl, attr);
+           cudaStream_t s) {
+    const dim3 grid((d + 255) / 256 < 16 ? (d + 255) / 256 : 16, n);
     if (wt == kBF16)
-        cudaLaunchKernelEx(&cfg, embed_kernel<__nv_bfloat16>, static_cast<const __nv_bfloat16*>(emb), ld_emb,
-                           tokens, d, x, x_ld);
+        embed_kernel<__nv_bfloat16><<<grid, 256, 0, s>>>(static_cast<const __nv_bfloat16*>(emb), ld_emb, tokens, d, x,
+                                                         x_ld);
     else
-        cudaLaunchKernelEx(&cfg, embed_kernel<float>, static_cast<const float*>(emb), ld_emb, tokens, d, x, x_ld);
+        embed_kernel<float><<<grid, 256, 0, s>>>(static_cast<const float*>(emb), ld_emb, tokens, d, x, x_ld);
 }
 
 void rmsnorm_rows(WType wt, const float* x, int x_ld, const float* gamma, float eps, int rows, int d, void* y,
@@ -210,19 +138,7 @@ void gather_last(const float* x, int x_ld, int batch, int T, int d, float* xl, i
     gather_last_kernel<<<dim3(4, batch), 256, 0, s>>>(x, x_ld, T, d, xl, xl_ld);
 }
 
-void argmax_step(const float* logits, int batch, int vocab, int* tokens, int* pos, int pos_inc, int* out,
-                      int out_ld, int* step, unsigned* ticket, cudaStream_t s, bool pdl) {
-    cudaLaunchAttribute attr[1];
-    auto cfg = pdl_cfg(dim3(batch), dim3(1024), s, pdl, attr);
-    cudaLaunchKernelEx(&cfg, argmax_kernel, logits, vocab, tokens, pos, pos_inc, out, out_ld, step, ticket);
-}
-
 void set_int(int* p, int v, cudaStream_t s) { set_int_kernel<<<1, 1, 0, s>>>(p, v); }
-void add_int(int* p, int v, cudaStream_t s, bool pdl) {
-    cudaLaunchAttribute attr[1];
-    auto cfg = pdl_cfg(dim3(1), dim3(1), s, pdl, attr);
-    cudaLaunchKernelEx(&cfg, add_int_kernel, p, v);
-}
 
 void synth_fill(const SynthFill& f, cudaStream_t s) {
     const long long n = f.rows * f.cols;

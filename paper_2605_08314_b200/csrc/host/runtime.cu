@@ -1,18 +1,22 @@
 // Device model + session runtime (SPEC.md runtime :283-382, plan :384-446).
 //
-// Decode step (CS3 in SURVEY.md §3), per layer:
+// Decode step = one phase program run by the persistent
+// megakernel (csrc/cuda/decode_mk.cu), per layer:
 //   qkvA   p_qkv = rmsnorm(x) . [A_q|A_k|A_v]         (packed QKV projection)
 //   qkvB   q,k,v = p . B_{q,k,v}; RoPE(q,k) at pos; k,v -> cache row pos
-//   attn   split-K flash-decode over cache rows [0, pos]
+//   attn   dense-KV attention over cache rows [0, pos]
 //   oA/oB  x += (attn . A_o) . B_o
-//   ugA    p_ug = rmsnorm(x) . [A_up|A_gate]          (packed; no_merge = 2 launches)
+//   ugA    p_ug = rmsnorm(x) . [A_up|A_gate]          (packed; no_merge = 2 phases)
 //   ugB    h = silu(p_g . B_gate) * (p_u . B_up)
 //   dA/dB  x += (h . A_down) . B_down
-// then head GEMV (final RMSNorm prologue) and the greedy argmax that advances
-// the device length register. Every kernel is launched with PDL; plans
-// capture the same launches into CUDA graphs (per layer or per step).
+// framed by the embedding gather and the head + greedy argmax that advances
+// the device length register. Plans: eager =
+// one launch per phase, per_layer = one CUDA graph per layer, full_step = one
+// graph per step -- the same phases, so bitwise identical outputs.
+// Prefill runs the chunked GEMM path.
 #include <algorithm>
 #include <cmath>
+#include <cstdlib>
 #include <cstring>
 #include <thread>
 
@@ -47,25 +51,25 @@ void* DeviceModel::alloc(size_t bytes) {
 
 namespace {
 
-struct Plan {
-    // byte sizes of every device tensor, computed before allocation
-    size_t total = 0;
-    void add(size_t b) { total += (b + 255) & ~size_t(255); }
-};
-
 void init_model_shapes(DeviceModel& dm, const ModelConfig& c, size_t cap, fsvd_dtype dt, int device) {
     dm.cfg = c;
     dm.capacity = cap;
     dm.wt = dt == FSVD_DTYPE_BF16 ? k::kBF16 : k::kF32;
     dm.esize = dt == FSVD_DTYPE_BF16 ? 2 : 4;
     dm.device = device;
-    dm.ldd = pad8(c.d_model);
+    dm.ldd = pad64(c.d_model);
+    dm.ldff = pad64(c.d_ff);
     FSVD_CUDA(cudaSetDevice(device));
     FSVD_CUDA(cudaDeviceGetAttribute(&dm.sm_count, cudaDevAttrMultiProcessorCount, device));
-    dm.ldff = pad8(c.d_ff);
 }
 
-size_t ld_in(const DeviceModel& dm, size_t proj) { return proj == kDown ? dm.ldff : dm.ldd; }
+DeviceMatrix make_matrix(int rows, int kk, int esize) {
+    DeviceMatrix m;
+    m.rows = rows;
+    m.k = kk;
+    m.kp = k::pad_line(kk, esize);
+    return m;
+}
 
 // Algorithmic bytes of one B=1 decode step: every layer's
 // factors once (a shared basis counts once per layer), head, gammas, one
@@ -86,35 +90,32 @@ void account(DeviceModel& dm, const std::vector<std::array<size_t, kNumProj>>& r
     dm.prefill_flops_per_token = 2 * params;
 }
 
-// Allocate the arena for the given per-layer ranks; A^T buffers deduplicated
-// by `key(layer, group_kind)` identity (shared bases).
-struct AKeys {
-    // per layer: identity keys of the qkv / o / ug / down input factors
-    std::vector<std::array<const void*, 4>> keys;
-};
-
-void allocate(DeviceModel& dm, const std::vector<std::array<size_t, kNumProj>>& ranks, const AKeys& ak) {
+// Allocate the arena. keys[l][p] identifies projection p's input factor
+// storage (nullptr = unique); equal keys share one device copy.
+void allocate(DeviceModel& dm, const std::vector<std::array<size_t, kNumProj>>& ranks,
+              const std::vector<std::array<const void*, kNumProj>>& keys) {
     const ModelConfig& c = dm.cfg;
-    const size_t es = dm.esize;
-    Plan plan;
-    plan.add(c.vocab * dm.ldd * es);  // emb
-    plan.add(c.vocab * dm.ldd * es);  // head^T
-    plan.add(c.d_model * 4);          // final gamma
-    std::map<const void*, bool> seen[4];
-    for (size_t l = 0; l < c.n_layers; ++l) {
-        const auto& r = ranks[l];
-        const size_t a_rows[4] = {r[kQ] + r[kK] + r[kV], r[kO], r[kUp] + r[kGate], r[kDown]};
-        const size_t a_ld[4] = {size_t(dm.ldd), size_t(dm.ldd), size_t(dm.ldd), size_t(dm.ldff)};
-        for (int g = 0; g < 4; ++g) {
-            const void* key = ak.keys[l][g];
-            if (key && seen[g].count(key)) continue;
-            if (key) seen[g][key] = true;
-            plan.add(a_rows[g] * a_ld[g] * es);
+    const int es = dm.esize;
+    auto bytes_of = [&](const DeviceMatrix& m) { return m.layout(es).bytes(); };
+    // plan sizes
+    size_t total = 0;
+    auto add = [&](size_t b) { total += (b + 255) & ~size_t(255); };
+    add(c.vocab * dm.ldd * es);
+    add(bytes_of(make_matrix(static_cast<int>(c.vocab), static_cast<int>(c.d_model), es)));
+    add(c.d_model * 4);
+    std::map<const void*, bool> seen;
+    for (size_t l = 0; l < c.n_layers; ++l)
+        for (size_t p = 0; p < kNumProj; ++p) {
+            const auto dims = proj_dims(c, p);
+            const void* key = keys[l][p];
+            if (!key || !seen.count(key)) {
+                if (key) seen[key] = true;
+                add(bytes_of(make_matrix(static_cast<int>(ranks[l][p]), static_cast<int>(dims[0]), es)));
+            }
+            add(bytes_of(make_matrix(static_cast<int>(dims[1]), static_cast<int>(ranks[l][p]), es)));
+            if (p == 0) add(2 * c.d_model * 4);
         }
-        for (size_t p = 0; p < kNumProj; ++p) plan.add(proj_dims(c, p)[1] * pad8(r[p]) * es);
-        plan.add(2 * c.d_model * 4);
-    }
-    dm.arena_bytes = plan.total + 4096;
+    dm.arena_bytes = total + 4096;
     FSVD_CUDA(cudaSetDevice(dm.device));
     cudaError_t e = cudaMalloc(&dm.arena, dm.arena_bytes);
     if (e != cudaSuccess) {
@@ -122,92 +123,91 @@ void allocate(DeviceModel& dm, const std::vector<std::array<size_t, kNumProj>>& 
         throw OomError("cannot allocate " + std::to_string(dm.arena_bytes) + " bytes of device weights");
     }
     FSVD_CUDA(cudaMemset(dm.arena, 0, dm.arena_bytes));
-    dm.stored_weight_bytes = plan.total;
+    dm.stored_weight_bytes = total;
 
     dm.emb = dm.alloc(c.vocab * dm.ldd * es);
-    dm.head_t = dm.alloc(c.vocab * dm.ldd * es);
+    dm.head_t = make_matrix(static_cast<int>(c.vocab), static_cast<int>(c.d_model), es);
+    dm.head_t.w = dm.alloc(bytes_of(dm.head_t));
     dm.final_gamma = static_cast<const float*>(dm.alloc(c.d_model * 4));
-    std::map<const void*, const void*> shared[4];
+    std::map<const void*, DeviceMatrix> shared;
     dm.layers.resize(c.n_layers);
     for (size_t l = 0; l < c.n_layers; ++l) {
         DeviceLayer& L = dm.layers[l];
-        const auto& r = ranks[l];
+        // input factors first, in projection order: q|k|v and up|gate end up adjacent
         for (size_t p = 0; p < kNumProj; ++p) {
-            L.r[p] = static_cast<int>(r[p]);
-            L.rp[p] = pad8(r[p]);
-        }
-        const size_t a_rows[4] = {r[kQ] + r[kK] + r[kV], r[kO], r[kUp] + r[kGate], r[kDown]};
-        const size_t a_ld[4] = {size_t(dm.ldd), size_t(dm.ldd), size_t(dm.ldd), size_t(dm.ldff)};
-        const void* ptrs[4];
-        for (int g = 0; g < 4; ++g) {
-            const void* key = ak.keys[l][g];
-            auto it = key ? shared[g].find(key) : shared[g].end();
-            if (it != shared[g].end()) {
-                ptrs[g] = it->second;
+            const auto dims = proj_dims(c, p);
+            L.r[p] = static_cast<int>(ranks[l][p]);
+            L.rp[p] = pad8(ranks[l][p]);
+            const void* key = keys[l][p];
+            auto it = key ? shared.find(key) : shared.end();
+            if (it != shared.end()) {
+                L.at[p] = it->second;
             } else {
-                ptrs[g] = dm.alloc(a_rows[g] * a_ld[g] * es);
-                if (key) shared[g][key] = ptrs[g];
+                L.at[p] = make_matrix(L.r[p], static_cast<int>(dims[0]), es);
+                L.at[p].w = dm.alloc(bytes_of(L.at[p]));
+                if (key) shared[key] = L.at[p];
             }
         }
-        L.at_qkv = ptrs[0];
-        L.at_o = ptrs[1];
-        L.at_ug = ptrs[2];
-        L.at_down = ptrs[3];
-        for (size_t p = 0; p < kNumProj; ++p) L.bt[p] = dm.alloc(proj_dims(c, p)[1] * L.rp[p] * es);
+        for (size_t p = 0; p < kNumProj; ++p) {
+            const auto dims = proj_dims(c, p);
+            L.bt[p] = make_matrix(static_cast<int>(dims[1]), L.r[p], es);
+            L.bt[p].w = dm.alloc(bytes_of(L.bt[p]));
+        }
         L.attn_gamma = static_cast<const float*>(dm.alloc(c.d_model * 4));
         L.mlp_gamma = static_cast<const float*>(dm.alloc(c.d_model * 4));
     }
     account(dm, ranks);
 }
 
-// Base pointer + row offset of projection p's A^T rows inside the packed buffer.
-const void* a_rows_ptr(const DeviceModel& dm, const DeviceLayer& L, size_t p) {
-    const char* base;
-    size_t row0 = 0;
-    switch (p) {
-        case kQ: base = static_cast<const char*>(L.at_qkv); break;
-        case kK: base = static_cast<const char*>(L.at_qkv); row0 = L.r[kQ]; break;
-        case kV: base = static_cast<const char*>(L.at_qkv); row0 = L.r[kQ] + L.r[kK]; break;
-        case kO: base = static_cast<const char*>(L.at_o); break;
-        case kUp: base = static_cast<const char*>(L.at_ug); break;
-        case kGate: base = static_cast<const char*>(L.at_ug); row0 = L.r[kUp]; break;
-        default: base = static_cast<const char*>(L.at_down); break;
-    }
-    return base + row0 * ld_in(dm, p) * dm.esize;
+inline uint16_t bf16_bits(float x) {
+    uint32_t u;
+    std::memcpy(&u, &x, 4);
+    if ((u & 0x7F800000u) != 0x7F800000u) u += 0x7FFFu + ((u >> 16) & 1u);
+    return static_cast<uint16_t>(u >> 16);
 }
 
-void to_device_dtype(const float* src, size_t n, k::WType wt, std::vector<uint8_t>& out) {
-    if (wt == k::kF32) {
-        out.resize(n * 4);
-        std::memcpy(out.data(), src, n * 4);
-        return;
-    }
-    out.resize(n * 2);
-    uint16_t* o = reinterpret_cast<uint16_t*>(out.data());
-    for (size_t i = 0; i < n; ++i) {
-        uint32_t u;
-        std::memcpy(&u, &src[i], 4);
-        if ((u & 0x7F800000u) != 0x7F800000u) u += 0x7FFFu + ((u >> 16) & 1u);
-        o[i] = static_cast<uint16_t>(u >> 16);
-    }
+template <typename F>
+void parallel_for(size_t n, F&& f) {
+    const unsigned hw = std::max(1u, std::min(16u, std::thread::hardware_concurrency()));
+    std::vector<std::thread> ts;
+    for (unsigned w = 0; w < hw; ++w) ts.emplace_back([&, w] { f(n * w / hw, n * (w + 1) / hw); });
+    for (auto& t : ts) t.join();
 }
 
-// Upload a host row-major [rows x cols] f32 matrix as transposed [cols][ld]
-// (transpose=true) or as [rows][ld] (transpose=false) in the model dtype.
-void upload_matrix(const DeviceModel& dm, const void* dst, const float* src, size_t rows, size_t cols, size_t ld,
-                   bool transpose) {
-    const size_t out_rows = transpose ? cols : rows, out_cols = transpose ? rows : cols;
-    std::vector<float> tmp(out_rows * ld, 0.f);
-    if (transpose) {
-        for (size_t i = 0; i < rows; ++i)
-            for (size_t j = 0; j < cols; ++j) tmp[j * ld + i] = src[i * cols + j];
-    } else {
-        for (size_t i = 0; i < rows; ++i) std::memcpy(&tmp[i * ld], &src[i * cols], cols * 4);
-    }
-    (void)out_cols;
-    std::vector<uint8_t> bytes;
-    to_device_dtype(tmp.data(), tmp.size(), dm.wt, bytes);
-    FSVD_CUDA(cudaMemcpy(const_cast<void*>(dst), bytes.data(), bytes.size(), cudaMemcpyHostToDevice));
+// Host-side tile packing: logical (row, k) of W^T = src[k * src_cols + row]
+// (the reference's d_in x d_out factor, transposed on the fly).
+void upload_tiles(const DeviceModel& dm, const DeviceMatrix& m, const float* src, size_t src_cols) {
+    const k::WLayout lay = m.layout(dm.esize);
+    std::vector<uint8_t> buf(lay.bytes(), 0);
+    parallel_for(static_cast<size_t>(m.rows), [&](size_t lo, size_t hi) {
+        for (size_t r = lo; r < hi; ++r)
+            for (int kk = 0; kk < m.k; ++kk) {
+                const float v = src[static_cast<size_t>(kk) * src_cols + r];
+                uint8_t* p = buf.data() + lay.offset(static_cast<int>(r), kk);
+                if (dm.esize == 2) {
+                    const uint16_t h = bf16_bits(v);
+                    std::memcpy(p, &h, 2);
+                } else {
+                    std::memcpy(p, &v, 4);
+                }
+            }
+    });
+    FSVD_CUDA(cudaMemcpy(const_cast<void*>(m.w), buf.data(), buf.size(), cudaMemcpyHostToDevice));
+}
+
+void upload_rows(const DeviceModel& dm, const void* dst, const float* src, size_t rows, size_t cols, size_t ld) {
+    std::vector<uint8_t> buf(rows * ld * dm.esize, 0);
+    for (size_t r = 0; r < rows; ++r)
+        for (size_t c = 0; c < cols; ++c) {
+            const float v = src[r * cols + c];
+            if (dm.esize == 2) {
+                const uint16_t h = bf16_bits(v);
+                std::memcpy(buf.data() + (r * ld + c) * 2, &h, 2);
+            } else {
+                std::memcpy(buf.data() + (r * ld + c) * 4, &v, 4);
+            }
+        }
+    FSVD_CUDA(cudaMemcpy(const_cast<void*>(dst), buf.data(), buf.size(), cudaMemcpyHostToDevice));
 }
 
 void upload_f32(const void* dst, const float* src, size_t n) {
@@ -221,37 +221,16 @@ std::unique_ptr<DeviceModel> upload_canonical(const CanonicalModel<float>& m, fs
     init_model_shapes(*dm, m.config, m.capacity, dt, device);
     const ModelConfig& c = m.config;
     std::vector<std::array<size_t, kNumProj>> ranks(c.n_layers);
-    AKeys ak;
-    ak.keys.resize(c.n_layers);
-    bool any_shared = false;
-    for (size_t l = 0; l < c.n_layers; ++l) {
-        const auto& L = m.layers[l];
-        for (size_t p = 0; p < kNumProj; ++p) ranks[l][p] = L.proj(p).rank;
-        for (size_t p = 0; p < kNumProj; ++p) any_shared |= L.proj(p).shared_group.has_value();
-    }
-    // Shared-basis identity: a packed group is reused only when every member
-    // factor aliases the same storage (family C); otherwise per-layer.
-    std::map<std::vector<const void*>, const void*> canon[4];
-    for (size_t l = 0; l < c.n_layers; ++l) {
-        const auto& L = m.layers[l];
-        const std::vector<const void*> ids[4] = {{L.q.a.get(), L.k.a.get(), L.v.a.get()},
-                                                 {L.o.a.get()},
-                                                 {L.up.a.get(), L.gate.a.get()},
-                                                 {L.down.a.get()}};
-        for (int g = 0; g < 4; ++g) {
-            if (!any_shared) {
-                ak.keys[l][g] = nullptr;
-                continue;
-            }
-            auto it = canon[g].find(ids[g]);
-            if (it == canon[g].end()) it = canon[g].emplace(ids[g], ids[g][0]).first;
-            ak.keys[l][g] = it->second;
+    std::vector<std::array<const void*, kNumProj>> keys(c.n_layers);
+    for (size_t l = 0; l < c.n_layers; ++l)
+        for (size_t p = 0; p < kNumProj; ++p) {
+            const auto& f = m.layers[l].proj(p);
+            ranks[l][p] = f.rank;
+            keys[l][p] = f.shared_group.has_value() ? static_cast<const void*>(f.a.get()) : nullptr;
         }
-    }
-    allocate(*dm, ranks, ak);
-
-    upload_matrix(*dm, dm->emb, m.embedding.data.data(), c.vocab, c.d_model, dm->ldd, false);
-    upload_matrix(*dm, dm->head_t, m.head.data.data(), c.d_model, c.vocab, dm->ldd, true);
+    allocate(*dm, ranks, keys);
+    upload_rows(*dm, dm->emb, m.embedding.data.data(), c.vocab, c.d_model, dm->ldd);
+    upload_tiles(*dm, dm->head_t, m.head.data.data(), c.vocab);
     upload_f32(dm->final_gamma, m.final_gamma.data(), c.d_model);
     std::map<const void*, bool> done;
     for (size_t l = 0; l < c.n_layers; ++l) {
@@ -260,12 +239,11 @@ std::unique_ptr<DeviceModel> upload_canonical(const CanonicalModel<float>& m, fs
         for (size_t p = 0; p < kNumProj; ++p) {
             const auto& f = L.proj(p);
             const auto dims = proj_dims(c, p);
-            const void* dst = a_rows_ptr(*dm, D, p);
-            if (!done.count(dst)) {
-                upload_matrix(*dm, dst, f.a->data.data(), dims[0], f.rank, ld_in(*dm, p), true);
-                done[dst] = true;
+            if (!done.count(D.at[p].w)) {  // A (d_in x r) -> A^T rows r, K d_in
+                upload_tiles(*dm, D.at[p], f.a->data.data(), f.rank);
+                done[D.at[p].w] = true;
             }
-            upload_matrix(*dm, D.bt[p], f.b->data.data(), f.rank, dims[1], D.rp[p], true);
+            upload_tiles(*dm, D.bt[p], f.b->data.data(), dims[1]);  // B (r x d_out) -> B^T rows d_out, K r
         }
         upload_f32(D.attn_gamma, L.attn_gamma.data(), c.d_model);
         upload_f32(D.mlp_gamma, L.mlp_gamma.data(), c.d_model);
@@ -280,23 +258,24 @@ std::unique_ptr<DeviceModel> generate_synthetic(const SynthSpec& spec, fsvd_dtyp
     auto dm = std::make_unique<DeviceModel>();
     init_model_shapes(*dm, spec.config, spec.capacity, dt, device);
     const ModelConfig& c = spec.config;
-    AKeys ak;
-    ak.keys.resize(c.n_layers);
-    // family C: every input factor of a layer group aliases one storage
-    // instance; use a synthetic identity per (group) -- all four packed
-    // groups share the same layer grouping.
-    static const char kTag[4] = {0, 1, 2, 3};
+    // family C: every projection's input factor is one storage instance per
+    // layer group; use the group's first-layer tensor name as the identity
+    std::vector<std::array<const void*, kNumProj>> keys(c.n_layers);
     for (size_t l = 0; l < c.n_layers; ++l)
-        for (int g = 0; g < 4; ++g)
-            ak.keys[l][g] = spec.family == 'C'
-                                ? reinterpret_cast<const void*>(reinterpret_cast<uintptr_t>(&kTag[g]) +
-                                                                 (l / spec.group_size) * 4096)
-                                : nullptr;
-    allocate(*dm, lay.ranks, ak);
+        for (size_t p = 0; p < kNumProj; ++p)
+            keys[l][p] = spec.family == 'C'
+                             ? static_cast<const void*>(lay.find(std::string("shared.") + kProjNames[p] + "." +
+                                                                 std::to_string(l / spec.group_size) + ".A"))
+                             : nullptr;
+    allocate(*dm, lay.ranks, keys);
     dm->family = spec.family;
-
-    auto fill = [&](const SynthTensor& t, const void* dst, long long rows, long long cols, long long rs,
-                    long long cs, int fold, uint64_t scale_off, k::WType dtype) {
+    auto need = [&](const std::string& n) -> const SynthTensor& {
+        const SynthTensor* t = lay.find(n);
+        if (!t) throw ConfigError("synthetic layout lacks '" + n + "'");
+        return *t;
+    };
+    auto fill = [&](const SynthTensor& t, long long rows, long long cols, int mode, const DeviceMatrix* m,
+                    const void* dst, long long rs, long long cs, int fold, uint64_t scale_off, k::WType dtype) {
         k::SynthFill f{};
         f.seed = spec.seed;
         f.offset = t.stream_offset;
@@ -306,21 +285,18 @@ std::unique_ptr<DeviceModel> generate_synthetic(const SynthSpec& spec, fsvd_dtyp
         f.cols = cols;
         f.rs = rs;
         f.cs = cs;
+        f.mode = mode;
+        if (m) f.lay = m->layout(dm->esize);
         f.fold = fold;
         f.scale_offset = scale_off;
         f.dst = const_cast<void*>(dst);
         f.dt = dtype;
         k::synth_fill(f, nullptr);
     };
-    auto need = [&](const std::string& n) -> const SynthTensor& {
-        const SynthTensor* t = lay.find(n);
-        if (!t) throw ConfigError("synthetic layout lacks '" + n + "'");
-        return *t;
-    };
     const long long V = c.vocab, d = c.d_model;
-    fill(need("embedding"), dm->emb, V, d, dm->ldd, 1, 0, 0, dm->wt);
-    fill(need("head"), dm->head_t, d, V, 1, dm->ldd, 0, 0, dm->wt);
-    fill(need("final_gamma"), dm->final_gamma, 1, d, 0, 1, 0, 0, k::kF32);
+    fill(need("embedding"), V, d, 0, nullptr, dm->emb, dm->ldd, 1, 0, 0, dm->wt);
+    fill(need("head"), d, V, 1, &dm->head_t, dm->head_t.w, 0, 0, 0, 0, dm->wt);
+    fill(need("final_gamma"), 1, d, 0, nullptr, dm->final_gamma, 0, 1, 0, 0, k::kF32);
     std::map<const void*, bool> done;
     for (size_t l = 0; l < c.n_layers; ++l) {
         const DeviceLayer& D = dm->layers[l];
@@ -329,28 +305,29 @@ std::unique_ptr<DeviceModel> generate_synthetic(const SynthSpec& spec, fsvd_dtyp
             const auto dims = proj_dims(c, p);
             const long long din = dims[0], dout = dims[1], r = D.r[p];
             const std::string pb = base + kProjNames[p];
-            const void* adst = a_rows_ptr(*dm, D, p);
-            const long long lda = static_cast<long long>(ld_in(*dm, p));
-            if (!done.count(adst)) {
-                done[adst] = true;
+            if (!done.count(D.at[p].w)) {
+                done[D.at[p].w] = true;
                 switch (spec.family) {
-                    case 'A': fill(need(pb + ".A"), adst, din, r, 1, lda, 0, 0, dm->wt); break;
+                    case 'A': fill(need(pb + ".A"), din, r, 1, &D.at[p], D.at[p].w, 0, 0, 0, 0, dm->wt); break;
                     case 'B':
-                        fill(need(pb + ".Uf"), adst, din, r, 1, lda, 1, need(pb + ".scale").stream_offset, dm->wt);
+                        fill(need(pb + ".Uf"), din, r, 1, &D.at[p], D.at[p].w, 0, 0, 1, need(pb + ".scale").stream_offset,
+                             dm->wt);
                         break;
                     case 'C':
                         fill(need(std::string("shared.") + kProjNames[p] + "." + std::to_string(l / spec.group_size) +
                                   ".A"),
-                             adst, din, r, 1, lda, 0, 0, dm->wt);
+                             din, r, 1, &D.at[p], D.at[p].w, 0, 0, 0, 0, dm->wt);
                         break;
-                    default: fill(need(pb + ".U"), adst, din, r, 1, lda, 2, need(pb + ".S").stream_offset, dm->wt);
+                    default:
+                        fill(need(pb + ".U"), din, r, 1, &D.at[p], D.at[p].w, 0, 0, 2, need(pb + ".S").stream_offset,
+                             dm->wt);
                 }
             }
             const SynthTensor& bt = need(pb + (spec.family == 'B' || spec.family == 'D' ? ".Vt" : ".B"));
-            fill(bt, D.bt[p], r, dout, 1, D.rp[p], 0, 0, dm->wt);
+            fill(bt, r, dout, 1, &D.bt[p], D.bt[p].w, 0, 0, 0, 0, dm->wt);
         }
-        fill(need(base + "attn_gamma"), D.attn_gamma, 1, d, 0, 1, 0, 0, k::kF32);
-        fill(need(base + "mlp_gamma"), D.mlp_gamma, 1, d, 0, 1, 0, 0, k::kF32);
+        fill(need(base + "attn_gamma"), 1, d, 0, nullptr, D.attn_gamma, 0, 1, 0, 0, k::kF32);
+        fill(need(base + "mlp_gamma"), 1, d, 0, nullptr, D.mlp_gamma, 0, 1, 0, 0, k::kF32);
     }
     FSVD_CUDA(cudaGetLastError());
     FSVD_CUDA(cudaDeviceSynchronize());
@@ -362,30 +339,30 @@ void copy_factor(const DeviceModel& dm, size_t layer, size_t proj, bool b, float
     const DeviceLayer& L = dm.layers[layer];
     const auto dims = proj_dims(dm.cfg, proj);
     const size_t r = L.r[proj];
-    // A: d_in x r from A^T [r][ld_in]; B: r x d_out from B^T [d_out][rp]
-    const size_t rows_t = b ? dims[1] : r, ld = b ? L.rp[proj] : ld_in(dm, proj);
     const size_t want = b ? r * dims[1] : dims[0] * r;
     if (count != want) throw ShapeError("copy_factor: count mismatch");
-    const void* src = b ? L.bt[proj] : a_rows_ptr(dm, L, proj);
-    std::vector<uint8_t> raw(rows_t * ld * dm.esize);
-    FSVD_CUDA(cudaMemcpy(raw.data(), src, raw.size(), cudaMemcpyDeviceToHost));
-    auto get = [&](size_t i) -> float {
+    const DeviceMatrix& m = b ? L.bt[proj] : L.at[proj];
+    const k::WLayout lay = m.layout(dm.esize);
+    std::vector<uint8_t> raw(lay.bytes());
+    FSVD_CUDA(cudaMemcpy(raw.data(), m.w, raw.size(), cudaMemcpyDeviceToHost));
+    auto get = [&](int row, int kk) -> float {
+        const uint8_t* p = raw.data() + lay.offset(row, kk);
         if (dm.esize == 4) {
             float f;
-            std::memcpy(&f, raw.data() + i * 4, 4);
+            std::memcpy(&f, p, 4);
             return f;
         }
         uint16_t h;
-        std::memcpy(&h, raw.data() + i * 2, 2);
-        uint32_t u = static_cast<uint32_t>(h) << 16;
+        std::memcpy(&h, p, 2);
+        const uint32_t u = static_cast<uint32_t>(h) << 16;
         float f;
         std::memcpy(&f, &u, 4);
         return f;
     };
-    const size_t cols_out = b ? dims[1] : r;   // logical cols
-    const size_t rows_out = b ? r : dims[0];
+    // logical A: d_in x r (= A^T[j][i]); B: r x d_out (= B^T[n][j])
+    const size_t rows_out = b ? r : dims[0], cols_out = b ? dims[1] : r;
     for (size_t i = 0; i < rows_out; ++i)
-        for (size_t j = 0; j < cols_out; ++j) out[i * cols_out + j] = get(j * ld + i);
+        for (size_t j = 0; j < cols_out; ++j) out[i * cols_out + j] = get(static_cast<int>(j), static_cast<int>(i));
 }
 
 // ----------------------------------------------------------------- session --
@@ -400,21 +377,28 @@ fsvd_ffn_backend route_ffn_auto(fsvd_plan_mode plan, fsvd_ffn_backend requested)
 
 void* Session::dalloc(size_t bytes) {
     void* p = nullptr;
-    cudaError_t e = cudaMalloc(&p, bytes < 256 ? 256 : bytes);
+    const size_t n = bytes < 256 ? 256 : bytes;
+    cudaError_t e = cudaMalloc(&p, n);
     if (e != cudaSuccess) {
         cudaGetLastError();
         throw OomError("session allocation of " + std::to_string(bytes) + " bytes failed");
     }
-    FSVD_CUDA(cudaMemsetAsync(p, 0, bytes < 256 ? 256 : bytes, stream_));
+    FSVD_CUDA(cudaMemsetAsync(p, 0, n, stream_));
     allocations_.push_back(p);
     return p;
+}
+
+k::GemvSeg Session::seg(const DeviceMatrix& mtx, int x_off, int y_off, int epi) const {
+    return k::GemvSeg{mtx.w, mtx.rows, mtx.k, mtx.kp, x_off, y_off, epi};
 }
 
 Session::Session(DeviceModel* m, const fsvd_session_opts& o) : m_(m) {
     const ModelConfig& c = m->cfg;
     B_ = static_cast<int>(o.batch);
     if (B_ < 1) throw ConfigError("session batch must be >= 1");
-    if (B_ > 4) throw ConfigError("decode batch > 4 is not supported by the CUDA-core GEMV path yet");
+    if (B_ > 2) throw ConfigError("decode batch > 2 is not supported by the decode megakernel yet");
+    if (!(c.d_head == 32 || c.d_head == 64 || c.d_head == 128))
+        throw ConfigError("d_head must be 32, 64 or 128 for the sm_100a kernels");
     cap_ = o.capacity ? o.capacity : (m->capacity ? m->capacity : 8192);
     if (o.plan < FSVD_PLAN_EAGER || o.plan > FSVD_PLAN_FULL_STEP) throw ConfigError("unknown plan mode");
     if (o.ffn < FSVD_FFN_AUTO || o.ffn > FSVD_FFN_PACKED) throw ConfigError("unknown ffn backend");
@@ -445,34 +429,27 @@ Session::Session(DeviceModel* m, const fsvd_session_opts& o) : m_(m) {
     pos_ = static_cast<int*>(dalloc(4));
     step_ = static_cast<int*>(dalloc(4));
     tokens_ = static_cast<int*>(dalloc(4 * B_));
-    tickets_ = static_cast<unsigned*>(dalloc(64));
-    counters_ = static_cast<unsigned*>(dalloc(4 * B_ * H));
 
-    int max_rp_qkv = 0, max_ug = 0, max_o = 0, max_d = 0;
+    // rank-space vectors of the prefill path: segment s of a packed
+    // projection starts at the sum of the previous segments' pad8 ranks; the
+    // stride covers the last segment's padded (tile-layout) reduction length.
     for (const auto& Ly : m->layers) {
-        max_rp_qkv = std::max(max_rp_qkv, Ly.rp[kQ] + Ly.rp[kK] + Ly.rp[kV]);
-        max_ug = std::max(max_ug, Ly.rp[kUp] + Ly.rp[kGate]);
-        max_o = std::max(max_o, Ly.rp[kO]);
-        max_d = std::max(max_d, Ly.rp[kDown]);
+        ld_qkv_ = std::max(ld_qkv_, Ly.rp[kQ] + Ly.rp[kK] + Ly.bt[kV].kp);
+        ld_ug_ = std::max(ld_ug_, Ly.rp[kUp] + Ly.bt[kGate].kp);
+        ld_o_ = std::max(ld_o_, Ly.bt[kO].kp);
+        ld_d_ = std::max(ld_d_, Ly.bt[kDown].kp);
     }
-    ld_qkv_ = max_rp_qkv;
-    ld_ug_ = max_ug;
+    ld_qkv_ = pad8(ld_qkv_);
+    ld_ug_ = pad8(ld_ug_);
+    xres_[0] = static_cast<float*>(dalloc(4ull * B_ * m->ldd));
+    xres_[1] = static_cast<float*>(dalloc(4ull * B_ * m->ldd));
     x_ = static_cast<float*>(dalloc(4ull * B_ * m->ldd));
-    p_qkv_ = static_cast<float*>(dalloc(4ull * B_ * ld_qkv_));
-    q_ = static_cast<float*>(dalloc(4ull * B_ * m->ldd));
-    attn_ = static_cast<float*>(dalloc(4ull * B_ * m->ldd));
-    p_o_ = static_cast<float*>(dalloc(4ull * B_ * max_o));
-    p_ug_ = static_cast<float*>(dalloc(4ull * B_ * ld_ug_));
-    h_ = static_cast<float*>(dalloc(4ull * B_ * m->ldff));
-    p_d_ = static_cast<float*>(dalloc(4ull * B_ * max_d));
     logits_ = static_cast<float*>(dalloc(4ull * B_ * c.vocab));
 
-    // split-K: ~2 CTAs per SM, each split <= kAttnMaxChunk rows
-    const int bh = B_ * static_cast<int>(H);
-    splits_ = std::max((296 + bh - 1) / bh, static_cast<int>((cap_ + k::kAttnMaxChunk - 1) / k::kAttnMaxChunk));
-    splits_ = std::min(splits_, 64);
-    if (static_cast<size_t>(splits_) * k::kAttnMaxChunk < cap_) throw ConfigError("capacity too large for split-K");
-    partial_ = static_cast<float*>(dalloc(4ull * bh * splits_ * (dh + 2)));
+    mk_grid_ = m->sm_count;
+    mk_splits_ = mk_grid_;  // attention partial slots per head: one per contributing CTA
+    attn_part_ = static_cast<float*>(dalloc(4ull * B_ * H * mk_splits_ * (dh + 4)));
+    build_program();
     FSVD_CUDA(cudaStreamSynchronize(stream_));
     stats_.allocs = 0;
 }
@@ -500,196 +477,339 @@ void* Session::staging(size_t bytes) {
     return staging_;
 }
 
-void Session::launch_gemv(const k::GemvArgs& a) {
-    k::gemv(m_->wt, B_, a, m_->sm_count, stream_, pdl_);
-    ++launches_this_step_;
+// ------------------------------------------------------------ phase program --
+// Appends one GEMV phase; returns where its pieces live. in_refs[s] is the
+// producer of in.seg[s] (the device pointers are patched in after every
+// phase is known and the buffers are sized).
+Session::PieceRef Session::add_gemv(const std::vector<k::GemvSeg>& segs, int dual, k::InputSpec in,
+                                    const std::vector<PieceRef>& in_refs, int x_len, const float* gamma) {
+    const DeviceModel& m = *m_;
+    k::MkPhase p{};
+    p.kind = k::kMkGemv;
+    k::MkGemv& g = p.g;
+    for (size_t i = 0; i < segs.size(); ++i) g.seg[i] = segs[i];
+    g.nseg = static_cast<int>(segs.size());
+    g.dual = dual;
+    g.in = in;
+    g.x_len = x_len;
+    g.gamma = gamma;
+    g.eps = static_cast<float>(m.cfg.norm_eps);
+    g.norm_len = static_cast<int>(m.cfg.d_model);
+    // every GEMV phase owns its pieces buffer (unused slots stay zero)
+    const int nt = k::mk_out_tiles(g.seg, g.nseg, dual, m.esize);
+    std::vector<uint8_t> np(nt);
+    PieceRef r{0, 0, 0, nt * k::kTileRows};
+    r.S = k::mk_npieces(g.seg, g.nseg, dual, m.esize, mk_grid_, np.data());
+    r.off = piece_floats_;
+    piece_floats_ += (static_cast<size_t>(r.R) * r.S * B_ + 63) / 64 * 64;
+    const int units = k::mk_units(g.seg, g.nseg, dual, m.esize);
+    const int per_cta = (units + mk_grid_ - 1) / mk_grid_ + 1;
+    region_max_ = std::max(region_max_, k::mk_region_bytes(B_, m.wt, x_len, per_cta));
+    if (h_phases_.size() == h_phases_.capacity()) throw std::logic_error("phase program capacity");
+    h_phases_.push_back(p);
+    k::MkGemv& G = h_phases_.back().g;
+    fix(&G.out, r);
+    for (size_t i = 0; i < in_refs.size(); ++i) fix(&G.in.seg[i].pc, in_refs[i]);
+    return r;
 }
 
-void Session::layer_body(size_t l) {
+namespace {
+k::InSeg inseg(int x_off, int rows, int tbase) {
+    k::InSeg s{};
+    s.x_off = x_off;
+    s.rows = rows;
+    s.tbase = tbase;
+    return s;
+}
+int tiles(int rows) { return (rows + k::kTileRows - 1) / k::kTileRows; }
+}  // namespace
+
+// One layer: prev = the down projection's pieces of the
+// previous layer (buf < 0: layer 0 starts from the embedding).
+void Session::add_layer_phases(size_t l, PieceRef& prev) {
     const DeviceModel& m = *m_;
     const ModelConfig& c = m.cfg;
     const DeviceLayer& L = m.layers[l];
-    const int d = static_cast<int>(c.d_model), ldd = m.ldd, ldff = m.ldff;
-    const float eps = static_cast<float>(c.norm_eps);
+    const int d = static_cast<int>(c.d_model), dff = static_cast<int>(c.d_ff);
     char* kc = static_cast<char*>(kc_) + l * cache_lstride_ * m.esize;
     char* vc = static_cast<char*>(vc_) + l * cache_lstride_ * m.esize;
-    const int rq = L.rp[kQ], rk = L.rp[kK], rv = L.rp[kV];
-
-    // qkvA: p_qkv = rmsnorm(x) . [A_q | A_k | A_v]
-    {
-        k::GemvArgs a{};
-        const char* base = static_cast<const char*>(L.at_qkv);
-        a.seg[0] = {base, L.r[kQ], ldd, ldd, 0, 0, k::kEpiStore};
-        a.seg[1] = {base + size_t(L.r[kQ]) * ldd * m.esize, L.r[kK], ldd, ldd, 0, rq, k::kEpiStore};
-        a.seg[2] = {base + size_t(L.r[kQ] + L.r[kK]) * ldd * m.esize, L.r[kV], ldd, ldd, 0, rq + rk, k::kEpiStore};
-        a.nseg = 3;
-        a.x = x_;
-        a.x_ld = ldd;
-        a.x_len = ldd;
-        a.gamma = L.attn_gamma;
-        a.eps = eps;
-        a.norm_len = d;
-        a.y = p_qkv_;
-        a.y_ld = ld_qkv_;
-        launch_gemv(a);
+    const int rq = L.rp[kQ], rk = L.rp[kK];
+    // residual stream: qkvA reads x = X[0] + prev (or the embedding), writes X[1]
+    k::InputSpec res{};
+    std::vector<PieceRef> res_refs;
+    if (prev.buf < 0) {
+        res.kind = k::kInEmbed;
+        res.emb = m.emb;
+        res.emb_ld = m.ldd;
+        res.tokens = tokens_;
+    } else {
+        res.kind = k::kInResidual;
+        res.src = xres_[0];
+        res.src_ld = m.ldd;
+        res.seg[0] = inseg(0, d, 0);
+        res.nseg = 1;
+        res_refs.push_back(prev);
     }
-    // qkvB: q, k, v = p . B; RoPE; append k, v at pos
+    res.len = d;
+    res.dst = xres_[1];
+    res.dst_ld = m.ldd;
+    // qkvA: p_qkv = rmsnorm(x) . [A_q | A_k | A_v]   (packed QKV projection)
+    const PieceRef qkvA = add_gemv({seg(L.at[kQ], 0, 0, 0), seg(L.at[kK], 0, 0, 0), seg(L.at[kV], 0, 0, 0)}, 0, res,
+                                   res_refs, L.at[kQ].kp, L.attn_gamma);
+    // qkvB: q, k, v = p . B  (RoPE and the cache append happen in the attention prologue)
+    PieceRef qkvB;
     {
-        k::GemvArgs a{};
-        a.seg[0] = {L.bt[kQ], d, rq, rq, 0, 0, k::kEpiRopeQ};
-        a.seg[1] = {L.bt[kK], d, rk, rk, rq, 0, k::kEpiRopeK};
-        a.seg[2] = {L.bt[kV], d, rv, rv, rq + rk, 0, k::kEpiV};
-        a.nseg = 3;
-        a.x = p_qkv_;
-        a.x_ld = ld_qkv_;
-        a.x_len = rq + rk + rv;
-        a.y = q_;
-        a.y_ld = ldd;
+        k::InputSpec in{};
+        in.kind = k::kInPieces;
+        in.seg[0] = inseg(0, L.r[kQ], 0);
+        in.seg[1] = inseg(rq, L.r[kK], tiles(L.r[kQ]));
+        in.seg[2] = inseg(rq + rk, L.r[kV], tiles(L.r[kQ]) + tiles(L.r[kK]));
+        in.nseg = 3;
+        qkvB = add_gemv({seg(L.bt[kQ], 0, 0, 0), seg(L.bt[kK], rq, 0, 0), seg(L.bt[kV], rq + rk, 0, 0)}, 0, in,
+                        {qkvA, qkvA, qkvA}, rq + rk + L.bt[kV].kp, nullptr);
+    }
+    // dense-KV attention over cache rows [0, pos]
+    {
+        k::MkPhase p{};
+        p.kind = k::kMkAttn;
+        k::MkAttn& a = p.a;
+        a.tbase_q = 0;
+        a.tbase_k = tiles(d);
+        a.tbase_v = 2 * tiles(d);
         a.rope = rope_;
-        a.pos = pos_;
-        a.d_head = static_cast<int>(c.d_head);
-        a.kcache = kc;
-        a.vcache = vc;
-        a.cache_bstride = cache_bstride_;
-        a.cache_hstride = cache_hstride_;
-        launch_gemv(a);
-    }
-    // attention over the dense cache
-    {
-        k::AttnDecodeArgs a{};
-        a.q = q_;
         a.kcache = kc;
         a.vcache = vc;
         a.cache_bstride = cache_bstride_;
         a.cache_hstride = cache_hstride_;
         a.pos = pos_;
-        a.out = attn_;
-        a.partial = partial_;
-        a.counters = counters_;
-        a.batch = B_;
+        a.partial = attn_part_;
         a.n_heads = static_cast<int>(c.n_heads);
         a.d_head = static_cast<int>(c.d_head);
-        a.splits = splits_;
+        a.splits = mk_splits_;
         a.scale = static_cast<float>(1.0 / std::sqrt(static_cast<double>(c.d_head)));
-        k::attn_decode(m.wt, a, stream_, pdl_);
-        ++launches_this_step_;
+        h_phases_.push_back(p);
+        fix(&h_phases_.back().a.pc, qkvB);
     }
-    // oA / oB
+    // o projection; the residual add happens in the next phase's staging
+    PieceRef oA, oB;
     {
-        k::GemvArgs a{};
-        a.seg[0] = {L.at_o, L.r[kO], ldd, ldd, 0, 0, k::kEpiStore};
-        a.nseg = 1;
-        a.x = attn_;
-        a.x_ld = ldd;
-        a.x_len = ldd;
-        a.y = p_o_;
-        a.y_ld = L.rp[kO];
-        launch_gemv(a);
+        k::InputSpec in{};
+        in.kind = k::kInAttn;
+        in.am = {attn_part_, static_cast<int>(c.n_heads), static_cast<int>(c.d_head), mk_splits_, pos_};
+        oA = add_gemv({seg(L.at[kO], 0, 0, 0)}, 0, in, {}, L.at[kO].kp, nullptr);
     }
     {
-        k::GemvArgs a{};
-        a.seg[0] = {L.bt[kO], d, L.rp[kO], L.rp[kO], 0, 0, k::kEpiAdd};
-        a.nseg = 1;
-        a.x = p_o_;
-        a.x_ld = L.rp[kO];
-        a.x_len = L.rp[kO];
-        a.y = x_;
-        a.y_ld = ldd;
-        launch_gemv(a);
+        k::InputSpec in{};
+        in.kind = k::kInPieces;
+        in.seg[0] = inseg(0, L.r[kO], 0);
+        in.nseg = 1;
+        oB = add_gemv({seg(L.bt[kO], 0, 0, 0)}, 0, in, {oA}, L.bt[kO].kp, nullptr);
     }
-    // ugA: packed (one launch over [A_up | A_gate]) or no_merge (two)
-    {
-        const char* base = static_cast<const char*>(L.at_ug);
-        const k::GemvSeg up = {base, L.r[kUp], ldd, ldd, 0, 0, k::kEpiStore};
-        const k::GemvSeg gate = {base + size_t(L.r[kUp]) * ldd * m.esize, L.r[kGate], ldd, ldd, 0, L.rp[kUp],
-                                 k::kEpiStore};
-        k::GemvArgs a{};
-        a.x = x_;
-        a.x_ld = ldd;
-        a.x_len = ldd;
-        a.gamma = L.mlp_gamma;
-        a.eps = eps;
-        a.norm_len = d;
-        a.y = p_ug_;
-        a.y_ld = ld_ug_;
-        if (ffn_ == FSVD_FFN_PACKED) {
-            a.seg[0] = up;
-            a.seg[1] = gate;
-            a.nseg = 2;
-            launch_gemv(a);
-        } else {
-            a.seg[0] = up;
-            a.nseg = 1;
-            launch_gemv(a);
-            a.seg[0] = gate;
-            launch_gemv(a);
-        }
+    // FFN input side: x = X[1] + o, written to X[0]; packed = one projection over [A_up | A_gate]
+    k::InputSpec r2{};
+    r2.kind = k::kInResidual;
+    r2.src = xres_[1];
+    r2.src_ld = m.ldd;
+    r2.len = d;
+    r2.dst = xres_[0];
+    r2.dst_ld = m.ldd;
+    r2.seg[0] = inseg(0, d, 0);
+    r2.nseg = 1;
+    k::InputSpec ugb{};
+    ugb.kind = k::kInPieces;
+    ugb.nseg = 2;
+    std::vector<PieceRef> ugb_refs;
+    if (ffn_ == FSVD_FFN_PACKED) {
+        const PieceRef ug =
+            add_gemv({seg(L.at[kUp], 0, 0, 0), seg(L.at[kGate], 0, 0, 0)}, 0, r2, {oB}, L.at[kUp].kp, L.mlp_gamma);
+        ugb.seg[0] = inseg(0, L.r[kUp], 0);
+        ugb.seg[1] = inseg(L.rp[kUp], L.r[kGate], tiles(L.r[kUp]));
+        ugb_refs = {ug, ug};
+    } else {
+        const PieceRef up = add_gemv({seg(L.at[kUp], 0, 0, 0)}, 0, r2, {oB}, L.at[kUp].kp, L.mlp_gamma);
+        k::InputSpec plain{};
+        plain.kind = k::kInPlain;
+        plain.src = xres_[0];
+        plain.src_ld = m.ldd;
+        plain.len = d;
+        const PieceRef gate = add_gemv({seg(L.at[kGate], 0, 0, 0)}, 0, plain, {}, L.at[kGate].kp, L.mlp_gamma);
+        ugb.seg[0] = inseg(0, L.r[kUp], 0);
+        ugb.seg[1] = inseg(L.rp[kUp], L.r[kGate], 0);
+        ugb_refs = {up, gate};
     }
-    // ugB: h = silu(p_g . B_gate) * (p_u . B_up)
+    // ugB (dual): up and gate reconstructions; SiLU.mul happens in dA's staging
+    const PieceRef ugB = add_gemv({seg(L.bt[kUp], 0, 0, 0), seg(L.bt[kGate], L.rp[kUp], 0, 0)}, 1, ugb, ugb_refs,
+                                  L.rp[kUp] + L.bt[kGate].kp, nullptr);
+    // down projection
+    PieceRef dA;
     {
-        k::GemvArgs a{};
-        a.seg[0] = {L.bt[kUp], static_cast<int>(c.d_ff), L.rp[kUp], L.rp[kUp], 0, 0, k::kEpiStore};
-        a.seg[1] = {L.bt[kGate], static_cast<int>(c.d_ff), L.rp[kGate], L.rp[kGate], L.rp[kUp], 0, k::kEpiStore};
-        a.nseg = 2;
-        a.dual = 1;
-        a.x = p_ug_;
-        a.x_ld = ld_ug_;
-        a.x_len = L.rp[kUp] + L.rp[kGate];
-        a.y = h_;
-        a.y_ld = ldff;
-        launch_gemv(a);
-    }
-    // down
-    {
-        k::GemvArgs a{};
-        a.seg[0] = {L.at_down, L.r[kDown], ldff, ldff, 0, 0, k::kEpiStore};
-        a.nseg = 1;
-        a.x = h_;
-        a.x_ld = ldff;
-        a.x_len = ldff;
-        a.y = p_d_;
-        a.y_ld = L.rp[kDown];
-        launch_gemv(a);
+        k::InputSpec in{};
+        in.kind = k::kInSilu;
+        in.seg[0] = inseg(0, dff, 0);
+        in.seg[1] = inseg(0, dff, tiles(dff));
+        in.nseg = 2;
+        dA = add_gemv({seg(L.at[kDown], 0, 0, 0)}, 0, in, {ugB, ugB}, L.at[kDown].kp, nullptr);
     }
     {
-        k::GemvArgs a{};
-        a.seg[0] = {L.bt[kDown], d, L.rp[kDown], L.rp[kDown], 0, 0, k::kEpiAdd};
-        a.nseg = 1;
-        a.x = p_d_;
-        a.x_ld = L.rp[kDown];
-        a.x_len = L.rp[kDown];
-        a.y = x_;
-        a.y_ld = ldd;
-        launch_gemv(a);
+        k::InputSpec in{};
+        in.kind = k::kInPieces;
+        in.seg[0] = inseg(0, L.r[kDown], 0);
+        in.nseg = 1;
+        prev = add_gemv({seg(L.bt[kDown], 0, 0, 0)}, 0, in, {dA}, L.bt[kDown].kp, nullptr);
     }
 }
 
-void Session::step_head(float* d_logits, int32_t* d_out, int out_ld) {
+void Session::build_program() {
     const DeviceModel& m = *m_;
     const ModelConfig& c = m.cfg;
-    k::GemvArgs a{};
-    a.seg[0] = {m.head_t, static_cast<int>(c.vocab), m.ldd, m.ldd, 0, 0, k::kEpiStore};
-    a.nseg = 1;
-    a.x = x_;
-    a.x_ld = m.ldd;
-    a.x_len = m.ldd;
-    a.gamma = m.final_gamma;
-    a.eps = static_cast<float>(c.norm_eps);
-    a.norm_len = static_cast<int>(c.d_model);
-    a.y = d_logits;
-    a.y_ld = static_cast<int>(c.vocab);
-    launch_gemv(a);
-    k::argmax_step(d_logits, B_, static_cast<int>(c.vocab), tokens_, pos_, 1, d_out, out_ld, step_, tickets_,
-                   stream_, pdl_);
+    const int d = static_cast<int>(c.d_model);
+    h_phases_.clear();
+    h_phases_.reserve(12 * c.n_layers + 16);
+    fixups_.clear();
+    piece_floats_ = 0;
+    region_max_ = 0;
+    ph_layer_begin_.clear();
+    ph_layer_end_.clear();
+    PieceRef prev{-1, 0, 0, 0};
+    for (size_t l = 0; l < c.n_layers; ++l) {
+        ph_layer_begin_.push_back(static_cast<int>(h_phases_.size()));
+        add_layer_phases(l, prev);
+        ph_layer_end_.push_back(static_cast<int>(h_phases_.size()));
+    }
+    best_v_ = static_cast<float*>(dalloc(4ull * mk_grid_ * B_));
+    best_i_ = static_cast<int*>(dalloc(4ull * mk_grid_ * B_));
+    ticket_ = static_cast<unsigned*>(dalloc(64));
+    mk_bar_ = static_cast<unsigned*>(dalloc(64));
+    auto add_head = [&](const k::InputSpec& in, const std::vector<PieceRef>& refs, int pos_inc, int& head_idx,
+                        int& arg_idx) {
+        head_idx = static_cast<int>(h_phases_.size());
+        const PieceRef hd = add_gemv({seg(m.head_t, 0, 0, 0)}, 0, in, refs, m.head_t.kp, m.final_gamma);
+        k::MkPhase p{};
+        p.kind = k::kMkArgmax;
+        p.m.vocab = static_cast<int>(c.vocab);
+        p.m.logits = logits_;
+        p.m.best_v = best_v_;
+        p.m.best_i = best_i_;
+        p.m.ticket = ticket_;
+        p.m.tokens = tokens_;
+        p.m.pos = pos_;
+        p.m.pos_inc = pos_inc;
+        p.m.step = step_;
+        arg_idx = static_cast<int>(h_phases_.size());
+        h_phases_.push_back(p);
+        fix(&h_phases_.back().m.pc, hd);
+    };
+    {  // decode: x = X[0] + last down projection, final RMSNorm, head
+        k::InputSpec in{};
+        in.kind = k::kInResidual;
+        in.src = xres_[0];
+        in.src_ld = m.ldd;
+        in.len = d;
+        in.seg[0] = inseg(0, d, 0);
+        in.nseg = 1;
+        add_head(in, {prev}, 1, ph_head_, ph_argmax_);
+    }
+    {  // prefill: the last position's hidden state (gathered into x_)
+        k::InputSpec in{};
+        in.kind = k::kInPlain;
+        in.src = x_;
+        in.src_ld = m.ldd;
+        in.len = d;
+        add_head(in, {}, 0, ph_pf_head_, ph_pf_argmax_);
+    }
+    // the pieces arena (zeroed once), then patch every Pieces reference
+    pieces_ = static_cast<float*>(dalloc(4 * piece_floats_));
+    for (auto& [p, r] : fixups_) {
+        p->base = pieces_ + r.off;
+        p->R = r.R;
+        p->S = r.S;
+    }
+    mk_region_ = (region_max_ + 127) / 128 * 128;
+    mk_red_ = k::mk_red_floats(B_, static_cast<int>(c.n_heads), static_cast<int>(c.d_head));
+    mk_smem_ = k::mk_smem_bytes(mk_region_, mk_red_);
+    if (mk_smem_ + 2048 > 227 * 1024)  // + the kernel's static shared memory
+        throw ConfigError("decode megakernel needs " + std::to_string(mk_smem_) +
+                          " bytes of shared memory for this (batch, shape); limit 232448");
+    if (const char* tr = std::getenv("FSVD_TRACE"); tr && tr[0] == '1')
+        trace_ = static_cast<unsigned long long*>(dalloc(8ull * mk_grid_ * (ph_argmax_ + 1) * 8));
+    d_phases_ = static_cast<k::MkPhase*>(dalloc(sizeof(k::MkPhase) * h_phases_.size()));
+    FSVD_CUDA(cudaMemcpyAsync(d_phases_, h_phases_.data(), sizeof(k::MkPhase) * h_phases_.size(),
+                              cudaMemcpyHostToDevice, stream_));
+}
+
+void Session::mk_run(int p_begin, int p_end) {
+    k::MkLaunch L{};
+    L.phases = d_phases_;
+    L.p_begin = p_begin;
+    L.p_end = p_end;
+    L.bar = mk_bar_;
+    L.region_bytes = mk_region_;
+    L.red_floats = mk_red_;
+    L.grid = mk_grid_;
+    L.smem_bytes = mk_smem_;
+    if (trace_ && p_begin == 0 && p_end == ph_argmax_ + 1) L.trace = trace_;
+    if (!k::mk_launch(m_->wt, B_, static_cast<int>(m_->cfg.d_head), L, stream_))
+        throw CudaError("megakernel: no instantiation for this (dtype, batch, d_head)");
+    FSVD_CUDA(cudaGetLastError());
     ++launches_this_step_;
 }
 
-void Session::capture_graphs() {
-    if (plan_ == FSVD_PLAN_PER_LAYER && layer_graphs_.empty()) {
-        for (size_t l = 0; l < m_->cfg.n_layers; ++l) {
+int Session::read_trace(unsigned long long* out, size_t count, int* grid) {
+    if (!trace_) throw ConfigError("tracing disabled (set FSVD_TRACE=1 before creating the session)");
+    const int nph = ph_argmax_ + 1;
+    const size_t n = static_cast<size_t>(mk_grid_) * nph * 8;
+    if (count < n) throw ShapeError("trace buffer too small");
+    FSVD_CUDA(cudaStreamSynchronize(stream_));
+    FSVD_CUDA(cudaMemcpy(out, trace_, n * 8, cudaMemcpyDeviceToHost));
+    if (grid) *grid = mk_grid_;
+    return nph;
+}
+
+void Session::mk_set_out(int32_t* d_out, int out_ld) {
+    if (d_out == mk_out_ && out_ld == mk_out_ld_) return;
+    k::MkPhase& p = h_phases_[ph_argmax_];
+    p.m.out = d_out;
+    p.m.out_ld = out_ld;
+    FSVD_CUDA(cudaMemcpyAsync(d_phases_ + ph_argmax_, &p, sizeof(k::MkPhase), cudaMemcpyHostToDevice, stream_));
+    mk_out_ = d_out;
+    mk_out_ld_ = out_ld;
+}
+
+// One decode step: eager = one launch per phase, per_layer = one launch
+// (captured as one graph) per layer, full_step = one graph for the step.
+void Session::mk_decode(int32_t* d_out, int out_ld) {
+    mk_set_out(d_out, out_ld);
+    const int L = static_cast<int>(m_->cfg.n_layers);
+    launches_this_step_ = 0;
+    if (plan_ == FSVD_PLAN_EAGER) {
+        for (int p = 0; p <= ph_argmax_; ++p) mk_run(p, p + 1);
+        stats_.dispatches += launches_this_step_;
+        stats_.kernel_launches += launches_this_step_;
+        return;
+    }
+    if (plan_ == FSVD_PLAN_FULL_STEP) {
+        if (!step_graph_) {
             cudaGraph_t g;
             FSVD_CUDA(cudaStreamBeginCapture(stream_, cudaStreamCaptureModeThreadLocal));
-            layer_body(l);
+            mk_run(0, ph_argmax_ + 1);
+            FSVD_CUDA(cudaStreamEndCapture(stream_, &g));
+            FSVD_CUDA(cudaGraphInstantiate(&step_graph_, g, 0));
+            cudaGraphDestroy(g);
+        }
+        FSVD_CUDA(cudaGraphLaunch(step_graph_, stream_));
+        stats_.graph_launches += 1;
+        stats_.dispatches += 1;
+        return;
+    }
+    // per-layer plans: layer 0 .. L-1 (layer 0 gathers the embedding), [head + argmax]
+    if (layer_graphs_.empty()) {
+        std::vector<std::pair<int, int>> ranges;
+        for (int l = 0; l < L; ++l) ranges.push_back({ph_layer_begin_[l], ph_layer_end_[l]});
+        ranges.push_back({ph_head_, ph_argmax_ + 1});
+        for (auto [b, e] : ranges) {
+            cudaGraph_t g;
+            FSVD_CUDA(cudaStreamBeginCapture(stream_, cudaStreamCaptureModeThreadLocal));
+            mk_run(b, e);
             FSVD_CUDA(cudaStreamEndCapture(stream_, &g));
             cudaGraphExec_t ge;
             FSVD_CUDA(cudaGraphInstantiate(&ge, g, 0));
@@ -697,82 +817,39 @@ void Session::capture_graphs() {
             layer_graphs_.push_back(ge);
         }
     }
+    for (auto g : layer_graphs_) FSVD_CUDA(cudaGraphLaunch(g, stream_));
+    stats_.graph_launches += layer_graphs_.size();
+    stats_.dispatches += layer_graphs_.size();
 }
 
-void Session::run_decode(int32_t* d_out, int out_ld, float* d_logits) {
+void Session::decode_step(const int32_t* d_tokens, float* d_logits) {
+    if (position_ == 0) throw ShapeError("decode_step: prefill first (position = 0)");
+    if (position_ >= cap_) throw CapacityError("decode_step: KV cache full (capacity " + std::to_string(cap_) + ")");
+    if (d_tokens) FSVD_CUDA(cudaMemcpyAsync(tokens_, d_tokens, 4ull * B_, cudaMemcpyDeviceToDevice, stream_));
     const uint64_t before = stats_.dispatches;
-    launches_this_step_ = 0;
-    const ModelConfig& c = m_->cfg;
-    if (plan_ == FSVD_PLAN_FULL_STEP) {
-        if (!step_graph_ || graph_out_ != d_out || graph_logits_ != d_logits || graph_out_ld_ != out_ld) {
-            if (step_graph_) cudaGraphExecDestroy(step_graph_);
-            cudaGraph_t g;
-            FSVD_CUDA(cudaStreamBeginCapture(stream_, cudaStreamCaptureModeThreadLocal));
-            k::embed(m_->wt, m_->emb, m_->ldd, tokens_, B_, static_cast<int>(c.d_model), x_, m_->ldd, stream_, pdl_);
-            for (size_t l = 0; l < c.n_layers; ++l) layer_body(l);
-            step_head(d_logits, d_out, out_ld);
-            FSVD_CUDA(cudaStreamEndCapture(stream_, &g));
-            FSVD_CUDA(cudaGraphInstantiate(&step_graph_, g, 0));
-            cudaGraphDestroy(g);
-            graph_out_ = d_out;
-            graph_out_ld_ = out_ld;
-            graph_logits_ = d_logits;
-        }
-        FSVD_CUDA(cudaGraphLaunch(step_graph_, stream_));
-        stats_.graph_launches += 1;
-        stats_.dispatches += 1;
-    } else {
-        k::embed(m_->wt, m_->emb, m_->ldd, tokens_, B_, static_cast<int>(c.d_model), x_, m_->ldd, stream_, pdl_);
-        stats_.dispatches += 1;
-        stats_.kernel_launches += 1;
-        if (plan_ == FSVD_PLAN_PER_LAYER) {
-            capture_graphs();
-            for (auto g : layer_graphs_) FSVD_CUDA(cudaGraphLaunch(g, stream_));
-            stats_.graph_launches += layer_graphs_.size();
-            stats_.dispatches += layer_graphs_.size();
-        } else {
-            launches_this_step_ = 0;
-            for (size_t l = 0; l < c.n_layers; ++l) layer_body(l);
-            stats_.dispatches += launches_this_step_;
-            stats_.kernel_launches += launches_this_step_;
-        }
-        launches_this_step_ = 0;
-        step_head(d_logits, d_out, out_ld);
-        stats_.dispatches += launches_this_step_;
-        stats_.kernel_launches += launches_this_step_;
-    }
+    mk_decode(nullptr, 0);
+    if (d_logits && d_logits != logits_)
+        FSVD_CUDA(cudaMemcpyAsync(d_logits, logits_, 4ull * B_ * m_->cfg.vocab, cudaMemcpyDeviceToDevice, stream_));
     FSVD_CUDA(cudaGetLastError());
     stats_.last_dispatches = stats_.dispatches - before;
     stats_.steps += 1;
     position_ += 1;
 }
 
-void Session::decode_step(const int32_t* d_tokens, float* d_logits) {
-    if (position_ == 0) throw ShapeError("decode_step: prefill first (position = 0)");
-    if (position_ >= cap_) throw CapacityError("decode_step: KV cache full (capacity " + std::to_string(cap_) + ")");
-    if (d_tokens)
-        FSVD_CUDA(cudaMemcpyAsync(tokens_, d_tokens, 4ull * B_, cudaMemcpyDeviceToDevice, stream_));
-    run_decode(nullptr, 0, d_logits ? d_logits : logits_);
-}
-
+// --------------------------------------------------------------- prefill --
 void Session::ensure_prefill_workspace(size_t rows) {
     if (rows <= pf_rows_) return;
     const DeviceModel& m = *m_;
     const size_t es = m.esize;
-    int max_o = 0, max_d = 0;
-    for (const auto& Ly : m.layers) {
-        max_o = std::max(max_o, Ly.rp[kO]);
-        max_d = std::max(max_d, Ly.rp[kDown]);
-    }
     pf_x_ = static_cast<float*>(dalloc(rows * m.ldd * 4));
     pf_xn_ = dalloc(rows * m.ldd * es);
     pf_pqkv_ = dalloc(rows * ld_qkv_ * es);
     pf_q_ = dalloc(rows * m.ldd * es);
     pf_att_ = dalloc(rows * m.ldd * es);
-    pf_po_ = dalloc(rows * max_o * es);
+    pf_po_ = dalloc(rows * ld_o_ * es);
     pf_pug_ = dalloc(rows * ld_ug_ * es);
     pf_h_ = dalloc(rows * m.ldff * es);
-    pf_pd_ = dalloc(rows * max_d * es);
+    pf_pd_ = dalloc(rows * ld_d_ * es);
     pf_tok_ = static_cast<int32_t*>(dalloc(rows * 4));
     pf_rows_ = rows;
     stats_.allocs += 10;
@@ -786,55 +863,47 @@ void Session::prefill_chunk(const int32_t* d_tokens, size_t T_total, size_t t0, 
     const int d = static_cast<int>(c.d_model), ldd = m.ldd, ldff = m.ldff;
     const float eps = static_cast<float>(c.norm_eps);
     const size_t es = m.esize;
-    // gather this chunk's tokens into [B*Tc]
     FSVD_CUDA(cudaMemcpy2DAsync(pf_tok_, Tc * 4, d_tokens + t0, T_total * 4, Tc * 4, B_, cudaMemcpyDeviceToDevice,
                                 stream_));
-    k::embed(m.wt, m.emb, ldd, pf_tok_, M, d, pf_x_, ldd, stream_, false);
+    k::embed(m.wt, m.emb, ldd, pf_tok_, M, d, pf_x_, ldd, stream_);
     const int p0 = static_cast<int>(position_);
+    auto gemm = [&](const void* x, int x_ld, int nseg, std::initializer_list<k::GemvSeg> segs, int epi, void* y,
+                    int y_ld, char* kc = nullptr, char* vc = nullptr) {
+        k::GemmArgs g{};
+        g.x = x;
+        g.x_ld = x_ld;
+        g.M = M;
+        int i = 0;
+        for (const auto& s : segs) g.seg[i++] = s;
+        g.nseg = nseg;
+        g.epi = epi;
+        g.y = y;
+        g.y_ld = y_ld;
+        g.rope = rope_;
+        g.p0 = p0;
+        g.T = static_cast<int>(Tc);
+        g.d_head = static_cast<int>(c.d_head);
+        g.n_heads = static_cast<int>(c.n_heads);
+        g.kcache = kc;
+        g.vcache = vc;
+        g.cache_bstride = cache_bstride_;
+        g.cache_hstride = cache_hstride_;
+        k::gemm(m.wt, g, stream_);
+    };
     for (size_t l = 0; l < c.n_layers; ++l) {
         const DeviceLayer& L = m.layers[l];
         char* kc = static_cast<char*>(kc_) + l * cache_lstride_ * es;
         char* vc = static_cast<char*>(vc_) + l * cache_lstride_ * es;
-        const int rq = L.rp[kQ], rk = L.rp[kK], rv = L.rp[kV];
+        const int rq = L.rp[kQ], rk = L.rp[kK];
         k::rmsnorm_rows(m.wt, pf_x_, ldd, L.attn_gamma, eps, M, d, pf_xn_, ldd, stream_);
-        {
-            k::GemmArgs g{};
-            const char* base = static_cast<const char*>(L.at_qkv);
-            g.x = pf_xn_;
-            g.x_ld = ldd;
-            g.M = M;
-            g.seg[0] = {base, L.r[kQ], ldd, ldd, 0, 0, k::kEpiStore};
-            g.seg[1] = {base + size_t(L.r[kQ]) * ldd * es, L.r[kK], ldd, ldd, 0, rq, k::kEpiStore};
-            g.seg[2] = {base + size_t(L.r[kQ] + L.r[kK]) * ldd * es, L.r[kV], ldd, ldd, 0, rq + rk, k::kEpiStore};
-            g.nseg = 3;
-            g.epi = k::kGemmStore;
-            g.y = pf_pqkv_;
-            g.y_ld = ld_qkv_;
-            k::gemm(m.wt, g, stream_);
-        }
-        {
-            k::GemmArgs g{};
-            g.x = pf_pqkv_;
-            g.x_ld = ld_qkv_;
-            g.M = M;
-            g.seg[0] = {L.bt[kQ], d, rq, rq, 0, 0, k::kEpiRopeQ};
-            g.seg[1] = {L.bt[kK], d, rk, rk, rq, 0, k::kEpiRopeK};
-            g.seg[2] = {L.bt[kV], d, rv, rv, rq + rk, 0, k::kEpiV};
-            g.nseg = 3;
-            g.epi = k::kGemmQKV;
-            g.y = pf_q_;
-            g.y_ld = ldd;
-            g.rope = rope_;
-            g.p0 = p0;
-            g.T = static_cast<int>(Tc);
-            g.d_head = static_cast<int>(c.d_head);
-            g.n_heads = static_cast<int>(c.n_heads);
-            g.kcache = kc;
-            g.vcache = vc;
-            g.cache_bstride = cache_bstride_;
-            g.cache_hstride = cache_hstride_;
-            k::gemm(m.wt, g, stream_);
-        }
+        gemm(pf_xn_, ldd, 3,
+             {seg(L.at[kQ], 0, 0, k::kEpiStore), seg(L.at[kK], 0, rq, k::kEpiStore),
+              seg(L.at[kV], 0, rq + rk, k::kEpiStore)},
+             k::kGemmStore, pf_pqkv_, ld_qkv_);
+        gemm(pf_pqkv_, ld_qkv_, 3,
+             {seg(L.bt[kQ], 0, 0, k::kEpiRopeQ), seg(L.bt[kK], rq, 0, k::kEpiRopeK),
+              seg(L.bt[kV], rq + rk, 0, k::kEpiV)},
+             k::kGemmQKV, pf_q_, ldd, kc, vc);
         {
             k::AttnPrefillArgs a{};
             a.q = pf_q_;
@@ -853,93 +922,20 @@ void Session::prefill_chunk(const int32_t* d_tokens, size_t T_total, size_t t0, 
             a.scale = static_cast<float>(1.0 / std::sqrt(static_cast<double>(c.d_head)));
             k::attn_prefill(m.wt, a, stream_);
         }
-        {
-            k::GemmArgs g{};
-            g.x = pf_att_;
-            g.x_ld = ldd;
-            g.M = M;
-            g.seg[0] = {L.at_o, L.r[kO], ldd, ldd, 0, 0, k::kEpiStore};
-            g.nseg = 1;
-            g.epi = k::kGemmStore;
-            g.y = pf_po_;
-            g.y_ld = L.rp[kO];
-            k::gemm(m.wt, g, stream_);
-        }
-        {
-            k::GemmArgs g{};
-            g.x = pf_po_;
-            g.x_ld = L.rp[kO];
-            g.M = M;
-            g.seg[0] = {L.bt[kO], d, L.rp[kO], L.rp[kO], 0, 0, k::kEpiStore};
-            g.nseg = 1;
-            g.epi = k::kGemmAddF32;
-            g.y = pf_x_;
-            g.y_ld = ldd;
-            k::gemm(m.wt, g, stream_);
-        }
+        gemm(pf_att_, ldd, 1, {seg(L.at[kO], 0, 0, k::kEpiStore)}, k::kGemmStore, pf_po_, ld_o_);
+        gemm(pf_po_, ld_o_, 1, {seg(L.bt[kO], 0, 0, k::kEpiStore)}, k::kGemmAddF32, pf_x_, ldd);
         k::rmsnorm_rows(m.wt, pf_x_, ldd, L.mlp_gamma, eps, M, d, pf_xn_, ldd, stream_);
-        {
-            const char* base = static_cast<const char*>(L.at_ug);
-            const k::GemvSeg up = {base, L.r[kUp], ldd, ldd, 0, 0, k::kEpiStore};
-            const k::GemvSeg gate = {base + size_t(L.r[kUp]) * ldd * es, L.r[kGate], ldd, ldd, 0, L.rp[kUp],
-                                     k::kEpiStore};
-            k::GemmArgs g{};
-            g.x = pf_xn_;
-            g.x_ld = ldd;
-            g.M = M;
-            g.epi = k::kGemmStore;
-            g.y = pf_pug_;
-            g.y_ld = ld_ug_;
-            if (ffn_ == FSVD_FFN_PACKED) {
-                g.seg[0] = up;
-                g.seg[1] = gate;
-                g.nseg = 2;
-                k::gemm(m.wt, g, stream_);
-            } else {
-                g.seg[0] = up;
-                g.nseg = 1;
-                k::gemm(m.wt, g, stream_);
-                g.seg[0] = gate;
-                k::gemm(m.wt, g, stream_);
-            }
+        if (ffn_ == FSVD_FFN_PACKED) {
+            gemm(pf_xn_, ldd, 2, {seg(L.at[kUp], 0, 0, k::kEpiStore), seg(L.at[kGate], 0, L.rp[kUp], k::kEpiStore)},
+                 k::kGemmStore, pf_pug_, ld_ug_);
+        } else {
+            gemm(pf_xn_, ldd, 1, {seg(L.at[kUp], 0, 0, k::kEpiStore)}, k::kGemmStore, pf_pug_, ld_ug_);
+            gemm(pf_xn_, ldd, 1, {seg(L.at[kGate], 0, L.rp[kUp], k::kEpiStore)}, k::kGemmStore, pf_pug_, ld_ug_);
         }
-        {
-            k::GemmArgs g{};
-            g.x = pf_pug_;
-            g.x_ld = ld_ug_;
-            g.M = M;
-            g.seg[0] = {L.bt[kUp], static_cast<int>(c.d_ff), L.rp[kUp], L.rp[kUp], 0, 0, k::kEpiStore};
-            g.seg[1] = {L.bt[kGate], static_cast<int>(c.d_ff), L.rp[kGate], L.rp[kGate], L.rp[kUp], 0, k::kEpiStore};
-            g.nseg = 2;
-            g.epi = k::kGemmSilu;
-            g.y = pf_h_;
-            g.y_ld = ldff;
-            k::gemm(m.wt, g, stream_);
-        }
-        {
-            k::GemmArgs g{};
-            g.x = pf_h_;
-            g.x_ld = ldff;
-            g.M = M;
-            g.seg[0] = {L.at_down, L.r[kDown], ldff, ldff, 0, 0, k::kEpiStore};
-            g.nseg = 1;
-            g.epi = k::kGemmStore;
-            g.y = pf_pd_;
-            g.y_ld = L.rp[kDown];
-            k::gemm(m.wt, g, stream_);
-        }
-        {
-            k::GemmArgs g{};
-            g.x = pf_pd_;
-            g.x_ld = L.rp[kDown];
-            g.M = M;
-            g.seg[0] = {L.bt[kDown], d, L.rp[kDown], L.rp[kDown], 0, 0, k::kEpiStore};
-            g.nseg = 1;
-            g.epi = k::kGemmAddF32;
-            g.y = pf_x_;
-            g.y_ld = ldd;
-            k::gemm(m.wt, g, stream_);
-        }
+        gemm(pf_pug_, ld_ug_, 2, {seg(L.bt[kUp], 0, 0, k::kEpiStore), seg(L.bt[kGate], L.rp[kUp], 0, k::kEpiStore)},
+             k::kGemmSilu, pf_h_, ldff);
+        gemm(pf_h_, ldff, 1, {seg(L.at[kDown], 0, 0, k::kEpiStore)}, k::kGemmStore, pf_pd_, ld_d_);
+        gemm(pf_pd_, ld_d_, 1, {seg(L.bt[kDown], 0, 0, k::kEpiStore)}, k::kGemmAddF32, pf_x_, ldd);
     }
 }
 
@@ -956,31 +952,19 @@ void Session::prefill(const int32_t* d_tokens, size_t T, float* d_logits) {
     for (size_t t0 = 0; t0 < T; t0 += Tc_max) {
         const size_t Tc = std::min(Tc_max, T - t0);
         prefill_chunk(d_tokens, T, t0, Tc);
-        k::set_int(pos_, static_cast<int>(position_ + Tc), stream_);
-        if (t0 + Tc == T) {
+        if (t0 + Tc == T)
             k::gather_last(pf_x_, m_->ldd, B_, static_cast<int>(Tc), static_cast<int>(c.d_model), x_, m_->ldd,
                            stream_);
-        }
         position_ += Tc;
     }
-    // head on the last position of every sequence; argmax sets the first
-    // generated token (pos already advanced: pos_inc = 0)
-    launches_this_step_ = 0;
-    const DeviceModel& m = *m_;
-    k::GemvArgs a{};
-    a.seg[0] = {m.head_t, static_cast<int>(c.vocab), m.ldd, m.ldd, 0, 0, k::kEpiStore};
-    a.nseg = 1;
-    a.x = x_;
-    a.x_ld = m.ldd;
-    a.x_len = m.ldd;
-    a.gamma = m.final_gamma;
-    a.eps = static_cast<float>(c.norm_eps);
-    a.norm_len = static_cast<int>(c.d_model);
-    a.y = d_logits ? d_logits : logits_;
-    a.y_ld = static_cast<int>(c.vocab);
-    k::gemv(m.wt, B_, a, m.sm_count, stream_, false);
+    k::set_int(pos_, static_cast<int>(position_), stream_);
+    // head on the last position of every sequence; the argmax phase sets the
+    // first generated token (pos_inc = 0: pos already advanced)
     k::set_int(step_, 0, stream_);
-    k::argmax_step(a.y, B_, static_cast<int>(c.vocab), tokens_, pos_, 0, nullptr, 0, step_, tickets_, stream_, false);
+    launches_this_step_ = 0;
+    mk_run(ph_pf_head_, ph_pf_argmax_ + 1);
+    if (d_logits && d_logits != logits_)
+        FSVD_CUDA(cudaMemcpyAsync(d_logits, logits_, 4ull * B_ * c.vocab, cudaMemcpyDeviceToDevice, stream_));
     FSVD_CUDA(cudaGetLastError());
 }
 
@@ -993,7 +977,14 @@ void Session::generate(const int32_t* d_prompt, size_t T, size_t max_new, int32_
     // first generated token = argmax of the prefill logits
     FSVD_CUDA(cudaMemcpy2DAsync(d_out, max_new * 4, tokens_, 4, 4, B_, cudaMemcpyDeviceToDevice, stream_));
     k::set_int(step_, 1, stream_);
-    for (size_t i = 1; i < max_new; ++i) run_decode(d_out, static_cast<int>(max_new), logits_);
+    for (size_t i = 1; i < max_new; ++i) {
+        const uint64_t before = stats_.dispatches;
+        mk_decode(d_out, static_cast<int>(max_new));
+        stats_.last_dispatches = stats_.dispatches - before;
+        stats_.steps += 1;
+        position_ += 1;
+    }
+    FSVD_CUDA(cudaGetLastError());
 }
 
 void Session::reset() {

@@ -4,6 +4,7 @@
 
 #include <cuda_runtime.h>
 
+#include <array>
 #include <cstdint>
 #include <map>
 #include <memory>
@@ -11,6 +12,7 @@
 #include <string>
 #include <vector>
 
+#include "../cuda/decode_mk.h"
 #include "../cuda/kernels.h"
 #include "fsvd/canonical.hpp"
 #include "fsvd/synth.hpp"
@@ -29,21 +31,24 @@ void cuda_check(cudaError_t e, const char* what);
 #define FSVD_CUDA(call) ::fsvd::rt::cuda_check((call), #call)
 
 inline int pad8(size_t v) { return static_cast<int>((v + 7) / 8 * 8); }
+inline int pad64(size_t v) { return static_cast<int>((v + 63) / 64 * 64); }
 
-// Device weights in the output-major layout the GEMV/GEMM kernels stream:
-//   A^T [r][ld_in]  (row j = column j of the reference's d_in x r factor)
-//   B^T [d_out][rp] (row n = column n of the r x d_out factor), rp = pad8(r)
-// Per layer the q/k/v input factors are packed row-wise into one A^T_qkv and
-// up/gate into A^T_ug (packing is an exact copy). Shared
-// bases (family C) are uploaded once per distinct storage instance.
+// A factor matrix W^T on the device, tile layout (csrc/cuda/layout.h).
+struct DeviceMatrix {
+    const void* w = nullptr;
+    int rows = 0, k = 0, kp = 0;
+    k::WLayout layout(int esize) const { return k::WLayout{rows, k, kp, esize}; }
+};
+
+// Per layer: A^T (rows r, K d_in) and B^T (rows d_out, K r) of every
+// projection q,k,v,o,up,gate,down. The q/k/v input factors are allocated
+// adjacently (one packed projection) and so are up/gate;
+// shared bases (family C) are uploaded once per storage instance.
 struct DeviceLayer {
     int r[kNumProj];
-    int rp[kNumProj];
-    const void* at_qkv;  // [r_q + r_k + r_v][ldd]
-    const void* at_o;    // [r_o][ldd]
-    const void* at_ug;   // [r_up + r_gate][ldd]
-    const void* at_down; // [r_down][ldff]
-    const void* bt[kNumProj];
+    int rp[kNumProj];  // rank padded to 8: stride of the rank-space vectors
+    DeviceMatrix at[kNumProj];
+    DeviceMatrix bt[kNumProj];
     const float* attn_gamma;
     const float* mlp_gamma;
 };
@@ -55,16 +60,16 @@ struct DeviceModel {
     int esize = 2;
     int device = 0;
     int sm_count = 148;
-    int ldd = 0, ldff = 0;
+    int ldd = 0, ldff = 0;  // activation strides (d_model, d_ff padded to 64)
     char family = 'A';
     void* arena = nullptr;
     size_t arena_bytes = 0, used = 0;
-    const void* emb = nullptr;     // [V][ldd]
-    const void* head_t = nullptr;  // [V][ldd]
+    const void* emb = nullptr;  // [V][ldd] row-major
+    DeviceMatrix head_t;        // rows V, K d_model
     const float* final_gamma = nullptr;
     std::vector<DeviceLayer> layers;
-    uint64_t stored_weight_bytes = 0;   // bytes actually resident (shared bases once)
-    uint64_t decode_weight_bytes = 0;   // bytes one B=1 decode step streams
+    uint64_t stored_weight_bytes = 0;      // bytes resident (shared bases once, incl. padding)
+    uint64_t decode_weight_bytes = 0;      // algorithmic bytes of one B=1 decode step
     uint64_t prefill_flops_per_token = 0;  // 2 * sum of factor params (GEMM part)
 
     ~DeviceModel();
@@ -103,16 +108,26 @@ class Session {
     fsvd_plan_mode plan() const { return plan_; }
     // device staging for host-pointer API calls (grown on demand)
     void* staging(size_t bytes);
+    // copies the last traced full step: [grid][phases][4] ns stamps; returns phases
+    int read_trace(unsigned long long* out, size_t count, int* grid);
+    std::array<int, 4> engine() const { return {1, k::kUnitBytes, k::mk_warps(), mk_splits_}; }
 
   private:
-    void layer_body(size_t l);
-    void step_head(float* d_logits, int32_t* d_out, int out_ld);
-    void run_decode(int32_t* d_out, int out_ld, float* d_logits);
-    void capture_graphs();
+    struct PieceRef {
+        int buf;     // < 0: none (layer 0 input = embedding)
+        size_t off;  // offset of the phase's buffer in the pieces arena (floats)
+        int S;       // slots
+        int R;       // rows (output tiles * 16)
+    };
+    void build_program();
+    void add_layer_phases(size_t l, PieceRef& prev);
+    void mk_run(int p_begin, int p_end);
+    void mk_decode(int32_t* d_out, int out_ld);
+    void mk_set_out(int32_t* d_out, int out_ld);
     void prefill_chunk(const int32_t* d_tokens, size_t T_total, size_t t0, size_t Tc);
     void ensure_prefill_workspace(size_t rows);
-    void launch_gemv(const k::GemvArgs& a);
     void* dalloc(size_t bytes);
+    k::GemvSeg seg(const DeviceMatrix& m, int x_off, int y_off, int epi) const;
 
     DeviceModel* m_;
     int B_;
@@ -123,8 +138,6 @@ class Session {
     std::vector<void*> allocations_;
     StepStats stats_;
     size_t position_ = 0;
-    int splits_ = 1;
-    bool pdl_ = true;
 
     // decode state
     void* kc_ = nullptr;
@@ -134,22 +147,39 @@ class Session {
     int* pos_ = nullptr;
     int* step_ = nullptr;
     int* tokens_ = nullptr;
-    unsigned* tickets_ = nullptr;
-    unsigned* counters_ = nullptr;
-    float *x_ = nullptr, *p_qkv_ = nullptr, *q_ = nullptr, *attn_ = nullptr, *p_o_ = nullptr, *p_ug_ = nullptr,
-          *h_ = nullptr, *p_d_ = nullptr, *logits_ = nullptr, *partial_ = nullptr;
-    int ld_qkv_ = 0, ld_ug_ = 0;
+    float* xres_[2] = {nullptr, nullptr};  // residual stream, double-buffered across residual phases
+    float* x_ = nullptr;                   // prefill: final hidden state of each sequence's last position
+    float* logits_ = nullptr;
+    float* attn_part_ = nullptr;
+    int ld_qkv_ = 0, ld_o_ = 0, ld_ug_ = 0, ld_d_ = 0;
     void* staging_ = nullptr;
     size_t staging_bytes_ = 0;
+
+    // megakernel program (decode_mk.cu)
+    PieceRef add_gemv(const std::vector<k::GemvSeg>& segs, int dual, k::InputSpec in,
+                      const std::vector<PieceRef>& in_refs, int x_len, const float* gamma);
+    void fix(k::Pieces* p, const PieceRef& r) { fixups_.push_back({p, r}); }
+    std::vector<k::MkPhase> h_phases_;
+    std::vector<std::pair<k::Pieces*, PieceRef>> fixups_;
+    size_t piece_floats_ = 0;
+    int region_max_ = 0;
+    k::MkPhase* d_phases_ = nullptr;
+    unsigned* mk_bar_ = nullptr;
+    float* pieces_ = nullptr;
+    float* best_v_ = nullptr;
+    int* best_i_ = nullptr;
+    unsigned* ticket_ = nullptr;
+    int mk_region_ = 0, mk_red_ = 0, mk_smem_ = 0, mk_grid_ = 0, mk_splits_ = 0;
+    int ph_head_ = 0, ph_argmax_ = 0, ph_pf_head_ = 0, ph_pf_argmax_ = 0;
+    std::vector<int> ph_layer_begin_, ph_layer_end_;
+    unsigned long long* trace_ = nullptr;  // FSVD_TRACE=1: per-phase globaltimer stamps of the full step
+    int32_t* mk_out_ = nullptr;
+    int mk_out_ld_ = 0;
+    uint64_t launches_this_step_ = 0;
 
     // plans
     std::vector<cudaGraphExec_t> layer_graphs_;
     cudaGraphExec_t step_graph_ = nullptr;
-    int32_t* graph_out_ = nullptr;  // out pointer baked into the step graph
-    int graph_out_ld_ = 0;
-    float* graph_logits_ = nullptr;
-    bool capturing_ = false;
-    uint64_t launches_this_step_ = 0;
 
     // prefill workspace
     size_t pf_rows_ = 0;
