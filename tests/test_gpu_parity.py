@@ -199,3 +199,47 @@ def test_dispatch_counts(fsvd):
     assert counts["full_step"] == 1
     assert counts["eager"] >= 5 * counts["full_step"]
     assert counts["full_step"] < counts["per_layer"] < counts["eager"]
+
+
+@pytest.mark.parametrize("dtype", ["f32", "bf16"])
+@pytest.mark.parametrize("fname", ["tiny_A.fsvd", "tiny_B.fsvd", "tiny_C.fsvd", "tiny_A_rho1.fsvd"])
+def test_reference_written_checkpoint(fsvd, oracle_mod, dtype, fname):
+    """FSVD15 files written by the reference's own compressor (tests/golden,
+    make_golden.py) through fsvd_model_load on the GPU vs the oracle on the
+    same file; rho=1 also vs the reference's dense_forward_all logits."""
+    import json
+
+    from conftest import GOLDEN
+
+    exp = json.loads((GOLDEN / "tiny_expect.json").read_text())
+    c = exp["config"]
+    cfg = fsvd.ModelConfig(c["n_layers"], c["d_model"], c["n_heads"], c["d_head"], c["d_ff"], c["vocab"])
+    toks = np.array(exp["tokens"], dtype=np.int32)
+    om = oracle_mod.OracleModel.load_file(GOLDEN / fname, cfg)
+    os_ = om.session(f64=True, capacity=64)
+    want = [os_.prefill(toks[:6])] + [os_.decode_step(int(t)) for t in toks[6:]]
+    model = fsvd.Model.load(GOLDEN / fname, dtype=dtype)
+    for plan in ("eager", "full_step"):
+        s = fsvd.Session(model, batch=1, capacity=64, plan=plan)
+        got = [s.prefill(toks[None, :6])[0]] + [s.decode_step([int(t)])[0] for t in toks[6:]]
+        assert oracle_mod.rel_err(np.stack(got), np.stack(want)) <= TOL[dtype], plan
+        if fname == "tiny_A_rho1.fsvd":
+            gold = np.load(GOLDEN / "tiny_dense_logits.npy")[5:]
+            assert oracle_mod.rel_err(np.stack(got), gold) <= TOL[dtype] + 1e-5
+
+
+def test_batch_prefill_decode_bf16_matches_oracle(fsvd, oracle_mod):
+    """B=4 independent sequences (continuous batching shape), bf16 tolerance."""
+    spec = _spec(fsvd, "C")
+    cfg = spec.config
+    prompt = _prompt(cfg, 23, batch=4, seed=11)
+    om = oracle_mod.OracleModel.synthetic(spec)
+    model = fsvd.Model.synthetic(spec, dtype="bf16")
+    s = fsvd.Session(model, batch=4, capacity=512, plan="full_step")
+    lp = s.prefill(prompt)
+    nxt = np.argmax(lp, axis=1).astype(np.int32)
+    ld = s.decode_step(nxt)
+    for b in range(4):
+        os_ = om.session(f64=True, capacity=512)
+        assert oracle_mod.rel_err(lp[b], os_.prefill(prompt[b])) <= 2e-2
+        assert oracle_mod.rel_err(ld[b], os_.decode_step(int(nxt[b]))) <= 2e-2
