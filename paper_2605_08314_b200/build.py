@@ -49,6 +49,7 @@ CUDA_SOURCES = [
     "cuda/decode_mk.cu",
     "cuda/attention.cu",
     "cuda/gemm_simt.cu",
+    "cuda/gemm_tc.cu",
     "cuda/gemm.cu",
     "cuda/misc.cu",
     "host/runtime.cu",

@@ -1,0 +1,381 @@
+// Prefill GEMM on the 5th-generation tensor cores (sm_100a, bf16 mode):
+//
+//   Y[t][n] = epi( sum_k X[t][k] * W^T[n][k] )      (SPEC.md:305-313 prefill:
+//   P = X.A once for the whole prompt, then P.B with the RoPE / KV-write,
+//   residual and SiLU.mul epilogues)
+//
+// One CTA per 128 x BN output tile, warp-specialized:
+//   warp 0      TMA producer: X tile (128 tokens x 64 k, SWIZZLE_128B) via a
+//               tensor map (cp.async.bulk.tensor.2d), W^T tile via BN/16
+//               contiguous 2 KiB cp.async.bulk copies -- the device weight
+//               layout (layout.h) already IS the K-major SWIZZLE_128B
+//               core-matrix image, so weights land in shared memory verbatim;
+//   warp 1      MMA issuer: one elected thread issues tcgen05.mma
+//               (kind::f16, M=128, N=BN, K=16) into a TMEM fp32 accumulator
+//               and tcgen05.commit's each stage back to the producer;
+//   warps 2..5  epilogue: tcgen05.ld 32 lanes x 32 columns per warp, then
+//               the fused epilogue straight from registers.
+// The dual (up/gate) GEMM runs the two K-loops into two TMEM accumulators and
+// applies silu(gate) * up in the epilogue, so up/gate never reach memory.
+#include <cuda.h>
+
+#include <stdexcept>
+#include <string>
+
+#include "common.cuh"
+#include "kernels.h"
+
+namespace fsvd::k {
+namespace {
+
+using namespace fsvd::dev;
+
+constexpr int BM = 128, BK = 64;
+constexpr int kABytes = BM * 128;  // 16 KiB: 128 rows x 128 B
+constexpr int kThreads = 192;
+
+template <int BN>
+struct Cfg {
+    static constexpr int kBBytes = BN * 128;
+    static constexpr int kStageBytes = kABytes + kBBytes;
+    static constexpr int kStages = (200 * 1024) / kStageBytes;
+    static constexpr int kSmem = kStages * kStageBytes + 1024 /*align*/ + 256 /*barriers*/;
+};
+
+struct TcArgs {
+    CUtensorMap xmap;  // X [rows][x_ld] bf16, box 64 x 128, SWIZZLE_128B
+    GemmArgs g;
+    int seg_tiles[3];  // BN-wide output tiles per segment
+};
+
+// ----------------------------------------------------------------- PTX ----
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+    return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+__device__ __forceinline__ void mbar_init(uint64_t* b, uint32_t count) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(b)), "r"(count));
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* b, uint32_t bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(b)), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* b, uint32_t parity) {
+    asm volatile(
+        "{\n"
+        ".reg .pred p;\n"
+        "WAIT_%=:\n"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+        "@!p bra WAIT_%=;\n"
+        "}\n" ::"r"(smem_u32(b)),
+        "r"(parity)
+        : "memory");
+}
+__device__ __forceinline__ void tma_load_2d(void* dst, const CUtensorMap* map, uint64_t* bar, int c0, int c1) {
+    asm volatile(
+        "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%3, %4}], [%2];" ::"r"(
+            smem_u32(dst)),
+        "l"(map), "r"(smem_u32(bar)), "r"(c0), "r"(c1)
+        : "memory");
+}
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
+    asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                     smem_u32(dst)),
+                 "l"(src), "r"(bytes), "r"(smem_u32(bar))
+                 : "memory");
+}
+__device__ __forceinline__ void tc_fence_after() { asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory"); }
+__device__ __forceinline__ void tc_fence_before() { asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory"); }
+__device__ __forceinline__ void tc_commit(uint64_t* bar) {
+    asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(smem_u32(bar))
+                 : "memory");
+}
+// D[tmem] (+)= A[smem] . B[smem]^T, bf16 in, fp32 accumulate
+__device__ __forceinline__ void tc_mma(uint32_t tmem_d, uint64_t da, uint64_t db, uint32_t idesc, uint32_t accum) {
+    asm volatile(
+        "{\n"
+        ".reg .pred p;\n"
+        "setp.ne.b32 p, %4, 0;\n"
+        "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n"
+        "}\n" ::"r"(tmem_d),
+        "l"(da), "l"(db), "r"(idesc), "r"(accum));
+}
+// K-major SWIZZLE_128B shared-memory matrix descriptor (8-row x 128 B atoms
+// stacked at 1024 B): start>>4 [0,14), LBO [16,30) (unused for SW128 K-major),
+// SBO>>4 [32,46), version 1 [46,48), layout SWIZZLE_128B = 2 [61,64).
+__device__ __forceinline__ uint64_t sw128_desc(uint32_t saddr) {
+    uint64_t d = static_cast<uint64_t>((saddr & 0x3FFFFu) >> 4);
+    d |= static_cast<uint64_t>(1) << 16;
+    d |= static_cast<uint64_t>(1024 >> 4) << 32;
+    d |= static_cast<uint64_t>(1) << 46;
+    d |= static_cast<uint64_t>(2) << 61;
+    return d;
+}
+// instruction descriptor, kind::f16: D f32, A/B bf16, both K-major
+template <int N>
+__device__ __forceinline__ constexpr uint32_t idesc_bf16() {
+    return (1u << 4) | (1u << 7) | (1u << 10) | (static_cast<uint32_t>(N >> 3) << 17) |
+           (static_cast<uint32_t>(BM >> 4) << 24);
+}
+__device__ __forceinline__ void tmem_ld32(uint32_t taddr, float (&v)[32]) {
+    uint32_t r[32];
+    asm volatile(
+        "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,%16,%17,%18,"
+        "%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];"
+        : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]), "=r"(r[8]),
+          "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15]), "=r"(r[16]),
+          "=r"(r[17]), "=r"(r[18]), "=r"(r[19]), "=r"(r[20]), "=r"(r[21]), "=r"(r[22]), "=r"(r[23]), "=r"(r[24]),
+          "=r"(r[25]), "=r"(r[26]), "=r"(r[27]), "=r"(r[28]), "=r"(r[29]), "=r"(r[30]), "=r"(r[31])
+        : "r"(taddr));
+    asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+#pragma unroll
+    for (int i = 0; i < 32; ++i) v[i] = __uint_as_float(r[i]);
+}
+
+__device__ __forceinline__ uint32_t pack_bf16(float a, float b) {
+    const __nv_bfloat162 h = __floats2bfloat162_rn(a, b);
+    return *reinterpret_cast<const uint32_t*>(&h);
+}
+// 32 consecutive bf16 outputs (64 B, 16 B aligned) from fp32 values
+__device__ __forceinline__ void store_bf16x32(__nv_bfloat16* dst, const float (&v)[32], int valid) {
+    if (valid >= 32 && (reinterpret_cast<uintptr_t>(dst) & 15) == 0) {
+        uint4* d4 = reinterpret_cast<uint4*>(dst);
+#pragma unroll
+        for (int q = 0; q < 4; ++q)
+            d4[q] = make_uint4(pack_bf16(v[8 * q + 0], v[8 * q + 1]), pack_bf16(v[8 * q + 2], v[8 * q + 3]),
+                               pack_bf16(v[8 * q + 4], v[8 * q + 5]), pack_bf16(v[8 * q + 6], v[8 * q + 7]));
+    } else {
+#pragma unroll
+        for (int i = 0; i < 32; ++i)
+            if (i < valid) dst[i] = __float2bfloat16_rn(v[i]);
+    }
+}
+
+// -------------------------------------------------------------- kernel ----
+template <int BN, bool DUAL>
+__global__ void __launch_bounds__(kThreads, 1) gemm_tc_kernel(const __grid_constant__ TcArgs A) {
+    using C = Cfg<BN>;
+    extern __shared__ __align__(1024) uint8_t smem_raw[];
+    uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+    uint64_t* full = reinterpret_cast<uint64_t*>(smem + C::kStages * C::kStageBytes);
+    uint64_t* empty = full + C::kStages;
+    uint64_t* tmem_full = empty + C::kStages;
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tmem_full + 1);
+
+    const GemmArgs& g = A.g;
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    // output tile -> (segment, n0)
+    int tile = blockIdx.y, s = 0;
+    if constexpr (!DUAL) {
+        while (s + 1 < g.nseg && tile >= A.seg_tiles[s]) {
+            tile -= A.seg_tiles[s];
+            ++s;
+        }
+    }
+    const GemvSeg& sg = g.seg[s];
+    const int n0 = tile * BN, m0 = blockIdx.x * BM;
+    constexpr int kAcc = DUAL ? 2 : 1;
+    constexpr uint32_t kCols = DUAL ? 2 * BN : BN;
+    constexpr uint32_t kAllocCols = kCols <= 32 ? 32 : kCols <= 64 ? 64 : kCols <= 128 ? 128 : kCols <= 256 ? 256 : 512;
+
+    if (threadIdx.x == 0) {
+        for (int i = 0; i < C::kStages; ++i) {
+            mbar_init(&full[i], 1);
+            mbar_init(&empty[i], 1);
+        }
+        mbar_init(tmem_full, 1);
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+        asm volatile("prefetch.tensormap [%0];" ::"l"(&A.xmap) : "memory");
+    }
+    if (warp == 0) {
+        asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_slot)),
+                     "r"(kAllocCols));
+        asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+    }
+    tc_fence_before();
+    __syncthreads();
+    tc_fence_after();
+    const uint32_t tmem_base = *tmem_slot;
+
+    // K-loop of accumulator j: segment, x column offset, k-blocks
+    auto seg_of = [&](int j) -> const GemvSeg& { return DUAL ? g.seg[j] : sg; };
+
+    if (warp == 0) {
+        if (lane == 0) {
+            int it = 0;
+#pragma unroll 1
+            for (int j = 0; j < kAcc; ++j) {
+                const GemvSeg& sj = seg_of(j);
+                const WLayout lay = sj.layout(2);
+                const int nk = lay.nlines();
+                const int t0 = n0 / 16;
+                const int nt = min(BN / 16, lay.ntiles() - t0);
+                const uint32_t bytes = kABytes + static_cast<uint32_t>(nt) * kLineTileBytes;
+                const char* wbase = static_cast<const char*>(sj.w) + static_cast<size_t>(t0) * lay.tile_bytes();
+#pragma unroll 1
+                for (int kb = 0; kb < nk; ++kb, ++it) {
+                    const int st = it % C::kStages;
+                    const uint32_t ph = (it / C::kStages) & 1;
+                    mbar_wait(&empty[st], ph ^ 1);
+                    uint8_t* sa = smem + st * C::kStageBytes;
+                    uint8_t* sb = sa + kABytes;
+                    mbar_expect_tx(&full[st], bytes);
+                    tma_load_2d(sa, &A.xmap, &full[st], sj.x_off + kb * BK, m0);
+                    const char* wl = wbase + static_cast<size_t>(kb) * kLineTileBytes;
+                    for (int i = 0; i < nt; ++i)
+                        bulk_g2s(sb + i * kLineTileBytes, wl + static_cast<size_t>(i) * lay.tile_bytes(),
+                                 kLineTileBytes, &full[st]);
+                }
+            }
+        }
+    } else if (warp == 1) {
+        if (lane == 0) {
+            constexpr uint32_t idesc = idesc_bf16<BN>();
+            int it = 0;
+#pragma unroll 1
+            for (int j = 0; j < kAcc; ++j) {
+                const int nk = seg_of(j).layout(2).nlines();
+                const uint32_t tacc = tmem_base + static_cast<uint32_t>(j * BN);
+#pragma unroll 1
+                for (int kb = 0; kb < nk; ++kb, ++it) {
+                    const int st = it % C::kStages;
+                    const uint32_t ph = (it / C::kStages) & 1;
+                    mbar_wait(&full[st], ph);
+                    tc_fence_after();
+                    const uint32_t sa = smem_u32(smem + st * C::kStageBytes);
+                    const uint32_t sb = sa + kABytes;
+                    const uint64_t da = sw128_desc(sa), db = sw128_desc(sb);
+#pragma unroll
+                    for (int k = 0; k < BK / 16; ++k)  // +32 B per K=16 step inside the 128 B swizzle atom
+                        tc_mma(tacc, da + 2 * k, db + 2 * k, idesc, (kb | k) != 0 ? 1u : 0u);
+                    tc_commit(&empty[st]);
+                }
+            }
+            tc_commit(tmem_full);
+        }
+    } else {
+        // epilogue: warp w reads TMEM lanes 32*(w%4) .. +31 (= tile rows)
+        const int q = warp & 3;
+        const int row = q * 32 + lane;
+        const int t = m0 + row;
+        mbar_wait(tmem_full, 0);
+        tc_fence_after();
+        const uint32_t lane_addr = tmem_base + (static_cast<uint32_t>(q * 32) << 16);
+#pragma unroll 1
+        for (int c0 = 0; c0 < BN; c0 += 32) {
+            float v[32], gt[32];
+            tmem_ld32(lane_addr + c0, v);  // .sync.aligned: every lane, before any divergence
+            if constexpr (DUAL) tmem_ld32(lane_addr + BN + c0, gt);
+            const int n = n0 + c0;
+            const int valid = min(32, sg.rows - n);
+            if (t >= g.M || valid <= 0) continue;
+            if constexpr (DUAL) {
+#pragma unroll
+                for (int i = 0; i < 32; ++i) v[i] = silu_mul(gt[i], v[i]);
+                store_bf16x32(static_cast<__nv_bfloat16*>(g.y) + static_cast<long long>(t) * g.y_ld + sg.y_off + n, v,
+                              valid);
+            } else if (g.epi == kGemmStore) {
+                store_bf16x32(static_cast<__nv_bfloat16*>(g.y) + static_cast<long long>(t) * g.y_ld + sg.y_off + n, v,
+                              valid);
+            } else if (g.epi == kGemmAddF32) {
+                float* y = static_cast<float*>(g.y) + static_cast<long long>(t) * g.y_ld + sg.y_off + n;
+#pragma unroll
+                for (int i = 0; i < 32; ++i)
+                    if (i < valid) y[i] += v[i];
+            } else {  // kGemmQKV: RoPE (interleaved pairs, math.hpp:30-44) + q store / KV append
+                const int b = t / g.T, pos = g.p0 + t % g.T;
+                if (sg.epi != kEpiV) {
+                    const float2* cs = g.rope + static_cast<long long>(pos) * (g.d_head / 2);
+#pragma unroll
+                    for (int i = 0; i < 32; i += 2) {
+                        const int ih = (n + i) % g.d_head;
+                        const float2 c = cs[ih >> 1];
+                        const float x0 = v[i], x1 = v[i + 1];
+                        v[i] = __fsub_rn(__fmul_rn(x0, c.x), __fmul_rn(x1, c.y));
+                        v[i + 1] = __fadd_rn(__fmul_rn(x0, c.y), __fmul_rn(x1, c.x));
+                    }
+                }
+                if (sg.epi == kEpiRopeQ) {
+                    store_bf16x32(static_cast<__nv_bfloat16*>(g.y) + static_cast<long long>(t) * g.y_ld + sg.y_off + n,
+                                  v, valid);
+                } else {
+                    const int h = n / g.d_head, ih = n % g.d_head;
+                    __nv_bfloat16* c = static_cast<__nv_bfloat16*>(sg.epi == kEpiRopeK ? g.kcache : g.vcache);
+                    store_bf16x32(c + b * g.cache_bstride + h * g.cache_hstride + static_cast<long long>(pos) * g.d_head +
+                                      ih,
+                                  v, valid);
+                }
+            }
+        }
+    }
+    tc_fence_before();
+    __syncthreads();
+    if (warp == 0) {
+        tc_fence_after();
+        asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem_base), "r"(kAllocCols));
+    }
+}
+
+// ------------------------------------------------------------ host side ----
+using EncodeTiled = CUresult (*)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
+                                 const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
+                                 CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+
+EncodeTiled encode_fn() {
+    static EncodeTiled fn = [] {
+        void* p = nullptr;
+        cudaDriverEntryPointQueryResult q;
+        if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) != cudaSuccess ||
+            q != cudaDriverEntryPointSuccess || !p)
+            throw std::runtime_error("cuTensorMapEncodeTiled unavailable");
+        return reinterpret_cast<EncodeTiled>(p);
+    }();
+    return fn;
+}
+
+template <int BN, bool DUAL>
+void launch(const TcArgs& ta, int tiles, int M, cudaStream_t s) {
+    using C = Cfg<BN>;
+    static bool attr = false;
+    if (!attr) {
+        cudaFuncSetAttribute(gemm_tc_kernel<BN, DUAL>, cudaFuncAttributeMaxDynamicSharedMemorySize, C::kSmem);
+        attr = true;
+    }
+    dim3 grid((M + BM - 1) / BM, tiles);
+    gemm_tc_kernel<BN, DUAL><<<grid, kThreads, C::kSmem, s>>>(ta);
+}
+
+}  // namespace
+
+bool gemm_tc_supported(const GemmArgs& a) {
+    // X row stride and segment offsets must allow 16 B-aligned TMA boxes
+    if (a.x_ld % 8) return false;
+    for (int i = 0; i < a.nseg; ++i)
+        if (a.seg[i].x_off % 8) return false;
+    return true;
+}
+
+void gemm_tc(const GemmArgs& a, int x_rows, cudaStream_t s) {
+    TcArgs ta{};
+    ta.g = a;
+    const cuuint64_t dims[2] = {static_cast<cuuint64_t>(a.x_ld), static_cast<cuuint64_t>(x_rows)};
+    const cuuint64_t strides[1] = {static_cast<cuuint64_t>(a.x_ld) * 2};
+    const cuuint32_t box[2] = {BK, BM};
+    const cuuint32_t estr[2] = {1, 1};
+    const CUresult r = encode_fn()(&ta.xmap, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(a.x), dims, strides,
+                                   box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                                   CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    if (r != CUDA_SUCCESS) throw std::runtime_error("cuTensorMapEncodeTiled failed: " + std::to_string(int(r)));
+    const bool dual = a.epi == kGemmSilu;
+    constexpr int BN = 128;
+    int tiles = 0;
+    const int nseg = dual ? 1 : a.nseg;
+    for (int i = 0; i < nseg; ++i) {
+        ta.seg_tiles[i] = (a.seg[i].rows + BN - 1) / BN;
+        tiles += ta.seg_tiles[i];
+    }
+    if (dual)
+        launch<BN, true>(ta, tiles, a.M, s);
+    else
+        launch<BN, false>(ta, tiles, a.M, s);
+}
+
+}  // namespace fsvd::k

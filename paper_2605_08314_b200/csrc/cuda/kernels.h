@@ -78,6 +78,9 @@ struct GemmArgs {
 };
 void gemm(WType wt, const GemmArgs& a, cudaStream_t s);       // dispatch: tcgen05 (bf16) / CUDA cores (f32)
 void gemm_simt(WType wt, const GemmArgs& a, cudaStream_t s);  // CUDA-core path
+// tcgen05/TMEM path (bf16): X is read through a TMA tensor map of x_rows rows
+bool gemm_tc_supported(const GemmArgs& a);
+void gemm_tc(const GemmArgs& a, int x_rows, cudaStream_t s);
 
 // ----------------------------------------------------------------- misc ----
 // x[b][:] = E[tokens[b]][:]  (fp32 out; E row-major [V][ld])

@@ -1,0 +1,4 @@
+nvcc -gencode arch=compute_100a,code=sm_100a -O2 -std=c++20 -I include tools/gemm_bench.cu -o /tmp/gemm_bench -L paper_2605_08314_b200 -lfsvd_b200 -Xlinker -rpath=$PWD/paper_2605_08314_b200 || exit 1
+for shp in "512 4096 4096" "512 3696 4096" "512 4096 1280" "512 1792 11008" "4096 4096 4096" "8192 8192 8192"; do
+  timeout 60 /tmp/gemm_bench $shp 20 2>&1 | tail -2
+done
