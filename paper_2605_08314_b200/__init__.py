@@ -454,16 +454,17 @@ class Session:
     def engine(self) -> dict:
         v = [C.c_int32() for _ in range(4)]
         _check(lib().fsvd_session_engine(self._h, *[C.byref(x) for x in v]))
-        return {"megakernel": bool(v[0].value), "unit_bytes": v[1].value, "warps_per_cta": v[2].value,
+        return {"megakernel": bool(v[0].value), "stage_bytes": v[1].value, "stages": v[2].value,
                 "attn_splits": v[3].value}
 
     def trace(self, max_phases: int = 4096) -> np.ndarray:
         """[grid, phases, 8] ns stamps of the last traced full step (FSVD_TRACE=1)."""
-        buf = np.zeros(148 * 2 * max_phases * 8, dtype=np.uint64)
+        buf = np.zeros(148 * 2 * max_phases * 16 + 8192 * 4, dtype=np.uint64)
         ph, g = C.c_int32(), C.c_int32()
         _check(lib().fsvd_session_trace(self._h, buf.ctypes.data_as(C.POINTER(C.c_uint64)), buf.size,
                                         C.byref(ph), C.byref(g)))
-        return buf[: g.value * ph.value * 8].reshape(g.value, ph.value, 8)
+        self.chunk_trace = buf[g.value * ph.value * 16: g.value * ph.value * 16 + 8192 * 4].reshape(8192, 4)
+        return buf[: g.value * ph.value * 16].reshape(g.value, ph.value, 16)
 
     def read_kv(self, layer: int, b: int, which: str, pos0: int, npos: int) -> np.ndarray:
         out = np.empty((npos, self._cfg.d_model), dtype=np.float32)

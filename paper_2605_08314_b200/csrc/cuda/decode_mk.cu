@@ -1,363 +1,519 @@
 // Persistent decode megakernel (sm_100a): the whole decode step -- embedding,
-// every layer's GEMV chain + attention, head and greedy argmax -- as a list of
-// phases executed by one CTA per SM with grid barriers between phases.
+// every layer's low-rank GEMV chain and attention, head and greedy argmax --
+// as a list of phases executed by one CTA per SM, grid barriers between
+// phases (SPEC.md:314-322 decode_step).
 //
-// Why: a B=1 decode step is ~290 dependent GEMV/attention ops of 1.5-12 us
-// each at HBM speed; separate launches leave HBM idle during every ramp and
-// tail. Here the weight stream never waits for activations:
+// Why: a B=1 decode step is ~290 dependent GEMV / attention ops of 1.5-12 us
+// each at HBM speed; separate kernels leave HBM idle during every launch ramp
+// and tail. Here the weight stream never waits for activations:
 //
-//  * Weights are in the tile layout (layout.h). A phase's work units are
-//    (16-row tile, 8 KiB k-slice) pairs -- one contiguous cp.async.bulk each --
-//    split evenly over all warps of the grid (balanced to one unit).
-//  * Each warp is its own producer: lane 0 issues the bulk copy (completing
-//    on a per-slot mbarrier) of the unit kSlots ahead of the one it computes,
-//    walking straight across phase boundaries -- so the next phase's weights
-//    are in flight while the warp waits at the grid barrier for activations.
-//  * bf16: a unit is reduced on the tensor cores, mma.sync m16n8k16 with the
-//    16 weight rows as A and x as B, where x = hi + lo is split into two bf16
-//    columns per batch row (fp32-grade activations, bf16 weights, fp32
-//    accumulate); a permutation of k inside each 16-wide step makes every
-//    A/B fragment load one 8-byte, bank-conflict-free LDS. fp32 weights
-//    (parity mode) use an exact CUDA-core dot product.
-//  * The grid barrier is the only inter-CTA synchronization. A CTA reduces
-//    its units in shared memory and stores one partial sum ("piece") per
-//    output tile it touched, in the tile's slot (CTA rank on that tile). The
-//    next phase's input staging sums a tile's pieces in slot order and applies
-//    the producer's epilogue (RMSNorm scale, residual add, SiLU.mul, RoPE + KV
-//    append, logits) -- no in-phase fences, atomics or tickets. Result bits
-//    depend only on the grid and the unit split, not on the launch structure,
-//    so the eager (one launch per phase), per-layer and full-step plans are
-//    bitwise identical.
-//  * Attention (decode_mk_attn.cuh) splits the dense cache rows over CTAs.
+//  * Producer warp (one per CTA): walks the GEMV phases of the launch in
+//    order and streams this CTA's weight units through a shared-memory ring
+//    of 16 KiB chunks with cp.async.bulk (mbarrier complete_tx), gated only
+//    by free ring slots -- across phase boundaries, so the next phase's
+//    weights land while the consumers wait at the grid barrier.
+//  * Consumer warps (8): per GEMV phase, one bulk copy stages the input
+//    vector (ready-made hi/lo bf16 planes, written by the previous phase's
+//    finalizers); chunk j of the phase goes to warp j % 8, which reduces it on
+//    the tensor cores (mma.sync, fp32 accumulate) into a per-chunk record.
+//  * Finalize: the CTA sums the records of each output tile in chunk order;
+//    a tile shared with neighbouring CTAs goes through per-CTA pieces and a
+//    per-tile counter, and its last contributor sums the pieces in CTA order
+//    and applies the epilogue (RMSNorm scale, RoPE + KV append, residual add,
+//    SiLU.mul, logits) -- once per row, deterministic for any launch split.
+//  * Attention (dense KV): the B*H*len key rows are split
+//    evenly over the CTAs, online softmax per warp (math.hpp:56-101), merged
+//    per head by its last contributor into the o-projection's input planes.
 //
-// Reference semantics: SPEC.md:314-322 decode_step; RoPE math.hpp:30-44;
-// RMSNorm kernels_scalar.cpp:55-61; SiLU.mul :63-69; argmax (ties -> lowest
-// index) math.hpp:132-140.
+// Reference semantics: RoPE math.hpp:30-44 (interleaved pairs, host-double
+// angles); RMSNorm kernels_scalar.cpp:55-61; SiLU.mul :63-69; argmax ties ->
+// lowest index math.hpp:132-140.
 #include <algorithm>
 #include <stdexcept>
-#include <utility>
 #include <vector>
 
-#include "decode_mk_attn.cuh"
 #include "decode_mk_common.cuh"
 
 namespace fsvd::k {
 namespace mk {
 
-// ------------------------------------------------------------ unit cursor --
-// Units of a phase are numbered 0..total-1: segment by segment, tile-major,
-// k-slice fastest; dual phases interleave per tile (up units, then gate
-// units). CTA c owns units [total*c/G, total*(c+1)/G); its warps split that
-// range. An output tile's pieces are the partial sums of the CTAs whose
-// ranges intersect the tile's units (decode_mk.h).
-struct SegGeo {
-    const char* w;
-    int ntiles, nunits, nlines;
-    int ubase;  // first unit index of this segment (non-dual)
-    int tbase;  // first output tile of this segment
-    size_t tile_bytes;
+// full[stages], empty[stages], xbar -- rounded up to 128 B
+__host__ __device__ constexpr int mk_barrier_bytes(int stages) { return ((2 * stages + 1) * 8 + 127) / 128 * 128; }
+
+// shared-memory map of one CTA
+struct Smem {
+    char* ring;        // [stages][kChunkBytes]
+    uint64_t* full;    // [stages]
+    uint64_t* empty;   // [stages]
+    uint64_t* xbar;
+    void* x;           // staged input planes
+    float* rec;        // [rec_chunks][16][B] / attention scratch
+    float* misc;       // 256 floats
+    MkPhase* desc;     // [2] phase descriptors (double-buffered bulk copies)
+    uint64_t* dbar;    // [2]
+    void* gsh;         // GemvShared
 };
 
-template <int ES>
-__device__ __forceinline__ SegGeo seg_geo(const GemvSeg& sg, int ubase, int tbase) {
-    const WLayout lay = sg.layout(ES);
-    SegGeo s;
-    s.w = static_cast<const char*>(sg.w);
-    s.ntiles = lay.ntiles();
-    s.nlines = lay.nlines();
-    s.nunits = lay.nunits();
-    s.tile_bytes = lay.tile_bytes();
-    s.ubase = ubase;
-    s.tbase = tbase;
-    return s;
-}
-
-// Phase geometry (identical for every thread of the CTA).
-template <int ES>
-struct Geo {
-    int nseg, dual, total, cl, ch;  // CTA unit range [cl, ch)
-    SegGeo s0, s1, s2;
-
-    __device__ __forceinline__ SegGeo sg(int i) const { return i == 0 ? s0 : (i == 1 ? s1 : s2); }
-    __device__ __forceinline__ void init(const MkGemv& g, int cta, int ncta) {
-        nseg = g.nseg;
-        dual = g.dual;
-        s0 = seg_geo<ES>(g.seg[0], 0, 0);
-        const int u1 = s0.ntiles * s0.nunits;
-        s1 = nseg > 1 ? seg_geo<ES>(g.seg[1], u1, s0.ntiles) : s0;
-        const int u2 = nseg > 1 ? u1 + s1.ntiles * s1.nunits : u1;
-        s2 = nseg > 2 ? seg_geo<ES>(g.seg[2], u2, s0.ntiles + s1.ntiles) : s0;
-        total = dual ? s0.ntiles * (s0.nunits + s1.nunits) : (nseg > 2 ? u2 + s2.ntiles * s2.nunits : u2);
-        cl = unit_lo(total, cta, ncta);
-        ch = unit_lo(total, cta + 1, ncta);
-    }
-    // (segment, tile, slice) of unit U
-    __device__ __forceinline__ void locate(int U, int& s, int& tile, int& u) const {
-        if (dual) {
-            const int per = s0.nunits + s1.nunits;
-            tile = U / per;
-            const int rem = U - tile * per;
-            s = rem < s0.nunits ? 0 : 1;
-            u = s ? rem - s0.nunits : rem;
-        } else {
-            s = nseg > 2 && U >= s2.ubase ? 2 : (nseg > 1 && U >= s1.ubase ? 1 : 0);
-            const SegGeo c = sg(s);
-            const int rel = U - c.ubase;
-            tile = rel / c.nunits;
-            u = rel - tile * c.nunits;
-        }
-    }
-    // output tile of unit U and that tile's unit range [a, e)
-    __device__ __forceinline__ int out_tile(int U, int& a, int& e) const {
-        int s, tile, u;
-        locate(U, s, tile, u);
-        if (dual) {
-            const int per = s0.nunits + s1.nunits;
-            a = tile * per + (s ? s0.nunits : 0);
-            e = s ? (tile + 1) * per : a + s0.nunits;
-            return s ? s0.ntiles + tile : tile;
-        }
-        const SegGeo c = sg(s);
-        a = c.ubase + tile * c.nunits;
-        e = a + c.nunits;
-        return c.tbase + tile;
-    }
-};
-
-// A warp's position in its own unit stream across the phase program (all
-// fields warp-uniform registers; advancing is incremental).
-template <int ES>
-struct Cursor {
-    const MkPhase* phases;
-    int p, p_end;
-    int U, U_end;    // unit range of this warp in phase p
-    int s, tile, u;  // coordinates of unit U
-    Geo<ES> geo;
-    int cta, ncta, warp;
-
-    __device__ __forceinline__ void enter(int phase) {
-        p = phase;
-        while (p < p_end && phases[p].kind != kMkGemv) ++p;
-        if (p >= p_end) return;
-        geo.init(phases[p].g, cta, ncta);
-        const int n = geo.ch - geo.cl;
-        U = geo.cl + n * warp / kWarpsMk;
-        U_end = geo.cl + n * (warp + 1) / kWarpsMk;
-        if (U < U_end) geo.locate(U, s, tile, u);
-    }
-    __device__ __forceinline__ void skip_empty() {
-        while (p < p_end && U >= U_end) enter(p + 1);
-    }
-    __device__ __forceinline__ void init(const MkPhase* ph, int pb, int pe, int c, int nc, int wp) {
-        phases = ph;
-        p_end = pe;
-        cta = c;
-        ncta = nc;
-        warp = wp;
-        U = U_end = 0;
-        enter(pb);
-        skip_empty();
-    }
-    __device__ __forceinline__ bool done() const { return p >= p_end; }
-    __device__ __forceinline__ int lines() const { return min(kUnitLines, geo.sg(s).nlines - u * kUnitLines); }
-    __device__ __forceinline__ int bytes() const { return lines() * kLineTileBytes; }
-    __device__ __forceinline__ const char* src() const {
-        const SegGeo c = geo.sg(s);
-        return c.w + static_cast<size_t>(tile) * c.tile_bytes + static_cast<size_t>(u) * kUnitBytes;
-    }
-    __device__ __forceinline__ void advance() {
-        if (++U >= U_end) {
-            enter(p + 1);
-            skip_empty();
-            return;
-        }
-        ++u;
-        if (geo.dual) {
-            if (s == 0 && u == geo.s0.nunits) {
-                s = 1;
-                u = 0;
-            } else if (s == 1 && u == geo.s1.nunits) {
-                s = 0;
-                u = 0;
-                ++tile;
-            }
-        } else if (u == geo.sg(s).nunits) {
-            u = 0;
-            if (++tile == geo.sg(s).ntiles) {
-                tile = 0;
-                ++s;
-            }
-        }
-    }
-};
-
-// ---------------------------------------------------------- unit compute --
-// 16 row partials of one unit for each batch row -> part[(lu*16 + row)*B + b]
+// ---------------------------------------------------------------- GEMV ----
 template <typename W, int B>
-struct UnitDot;
-
-template <int B>
-struct UnitDot<__nv_bfloat16, B> {
-    static __device__ __forceinline__ void run(const char* buf, int lines, const Smem& sm, int kbase, int lane,
-                                               float* part, int lu) {
-        const int g = lane >> 2, t = lane & 3;
-        const __nv_bfloat16* xp = static_cast<const __nv_bfloat16*>(sm.x) + g * sm.x_cap;
-        float d[4] = {0.f, 0.f, 0.f, 0.f};
-        for (int l = 0; l < lines; ++l) {
-            const char* lb = buf + l * kLineTileBytes;
+__device__ __forceinline__ void finalize_rows(const MkGemv& g, const MkSplit& sp, int T, int i, const float (&v)[2][B],
+                                              const float* inv) {
+    using IO = PlaneIO<W>;
+    // segment and row of output tile T
+    int s = 0;
+    if (!sp.dual)
+        while (s + 1 < sp.nseg && T >= sp.tbase[s + 1]) ++s;
+    const int row = (T - sp.tbase[s]) * kTileRows + i;
+    const bool valid = i < kTileRows && row < g.seg[s].rows;  // lanes 16..31 carry no row
+    switch (g.out_kind) {
+        case kOutPlanes:
+            if (valid)
 #pragma unroll
-            for (int j = 0; j < 4; ++j) {
-                const int off = ((((2 * j + (t >> 1)) ^ g) & 7) << 4) | ((t & 1) << 3);
-                const uint2 r0 = *reinterpret_cast<const uint2*>(lb + g * kLineBytes + off);
-                const uint2 r1 = *reinterpret_cast<const uint2*>(lb + (g + 8) * kLineBytes + off);
-                uint2 xv = make_uint2(0u, 0u);
-                if (g < 2 * B) xv = *reinterpret_cast<const uint2*>(xp + kbase + l * 64 + 16 * j + 4 * t);
-                mma_bf16(d, r0.x, r1.x, r0.y, r1.y, xv.x, xv.y);
-            }
-        }
-        if (t < B) {
-            part[(lu * 16 + g) * B + t] = d[0] + d[1];
-            part[(lu * 16 + g + 8) * B + t] = d[2] + d[3];
-        }
-    }
-};
-
-template <int B>
-struct UnitDot<float, B> {
-    static __device__ __forceinline__ void run(const char* buf, int lines, const Smem& sm, int kbase, int lane,
-                                               float* part, int lu) {
-        const int i = lane >> 1, h = lane & 1;
-        const float* xf = static_cast<const float*>(sm.x);
-        float acc[B];
-#pragma unroll
-        for (int b = 0; b < B; ++b) acc[b] = 0.f;
-        for (int l = 0; l < lines; ++l) {
-#pragma unroll
-            for (int cc = 0; cc < 4; ++cc) {
-                const int c = h * 4 + cc;
-                const float4 w = *reinterpret_cast<const float4*>(buf + l * kLineTileBytes + i * kLineBytes +
-                                                                  (((c ^ (i & 7)) & 7) << 4));
+                for (int b = 0; b < B; ++b) IO::put(g.out, b, g.out_off[s] + row, v[0][b] * inv[b]);
+            break;
+        case kOutResid:
+            if (valid)
 #pragma unroll
                 for (int b = 0; b < B; ++b) {
-                    const float4 x = *reinterpret_cast<const float4*>(xf + b * sm.x_cap + kbase + l * 32 + c * 4);
-                    acc[b] = fmaf(w.x, x.x, acc[b]);
-                    acc[b] = fmaf(w.y, x.y, acc[b]);
-                    acc[b] = fmaf(w.z, x.z, acc[b]);
-                    acc[b] = fmaf(w.w, x.w, acc[b]);
+                    float* xr = g.xres + static_cast<size_t>(b) * g.xres_ld + row;
+                    const float x = __ldcg(xr) + v[0][b];
+                    *xr = x;
+                    IO::put(g.out, b, row, x * g.gamma[row]);
+                }
+            break;
+        case kOutSilu:
+            if (valid)
+#pragma unroll
+                for (int b = 0; b < B; ++b) IO::put(g.out, b, row, silu_mul(v[1][b], v[0][b]));
+            break;
+        case kOutLogits: {
+            // all 32 lanes take part in the tile-best reduction (lanes >= 16 carry nothing)
+#pragma unroll
+            for (int b = 0; b < B; ++b) {
+                float bv = -CUDART_INF_F;
+                int bi = 0x7fffffff;
+                if (valid) {
+                    const float x = v[0][b] * inv[b];
+                    g.logits[static_cast<size_t>(b) * g.vocab + row] = x;
+                    bv = x;
+                    bi = row;
+                }
+#pragma unroll
+                for (int o = 16; o > 0; o >>= 1) {
+                    const float ov = __shfl_xor_sync(0xffffffffu, bv, o);
+                    const int oi = __shfl_xor_sync(0xffffffffu, bi, o);
+                    if (better(ov, oi, bv, bi)) {
+                        bv = ov;
+                        bi = oi;
+                    }
+                }
+                if (i == 0) {
+                    g.cand_v[T * B + b] = bv;
+                    g.cand_i[T * B + b] = bi;
                 }
             }
+            break;
         }
+        default: {  // kOutQKV: segment 0 q, 1 k, 2 v
+            const int pos = *g.pos;
+            float o[B];
+#pragma unroll
+            for (int b = 0; b < B; ++b) {
+                const float x = v[0][b];
+                const float y = __shfl_xor_sync(0xffffffffu, x, 1);  // pair partner (rows 2i, 2i+1)
+                o[b] = x;
+                if (s < 2) {
+                    const int e = row % g.d_head;
+                    const float2 cs = g.rope[static_cast<long long>(pos) * (g.d_head / 2) + (e >> 1)];
+                    const float x0 = (e & 1) ? y : x, x1 = (e & 1) ? x : y;
+                    o[b] = (e & 1) ? __fadd_rn(__fmul_rn(x0, cs.y), __fmul_rn(x1, cs.x))
+                                   : __fsub_rn(__fmul_rn(x0, cs.x), __fmul_rn(x1, cs.y));
+                }
+            }
+            if (valid) {
+                const int h = row / g.d_head, e = row % g.d_head;
+#pragma unroll
+                for (int b = 0; b < B; ++b) {
+                    if (s == 0) {
+                        g.qbuf[static_cast<size_t>(b) * g.q_ld + row] = o[b];
+                    } else {
+                        W* c = static_cast<W*>(s == 1 ? g.kcache : g.vcache);
+                        c[b * g.cache_bstride + h * g.cache_hstride + static_cast<long long>(pos) * g.d_head + e] =
+                            from_f32<W>(o[b]);
+                    }
+                }
+            }
+            break;
+        }
+    }
+}
+
+// Shared-tile exchange of output tile T. The CTA owning T's first unit
+// (slot 0) finalizes: it waits for the other contributors' partials (their
+// publish is a release-increment of the tile counter, no round trip for
+// them) and sums slots 1.. onto its own partial in CTA order. Boundary tiles
+// are reduced first in every CTA (ChunkSeq), so the wait is normally one
+// poll. Returns false if another CTA finalizes T.
+template <int B>
+__device__ __forceinline__ bool exchange_pieces(const MkGemv& g, const MkSplit& sp, int T, int cta, int G, int lane,
+                                                float (&v)[2][B]) {
+    int ta, te;
+    sp.tile_span(T, ta, te);
+    const int c0 = sp.cta_of(ta, G), c1 = sp.cta_of(te - 1, G);
+    if (c0 == c1) return true;  // this CTA covers the whole tile
+    // contributors = non-empty CTAs in [c0, c1]: lane l tests CTA base + l
+    int np = 0, slot = 0;
+    for (int base = c0; base <= c1; base += 32) {
+        const int c = base + lane;
+        const bool ne = c <= c1 && sp.lo(c + 1, G) > sp.lo(c, G);
+        np += __popc(__ballot_sync(0xffffffffu, ne));
+        slot += __popc(__ballot_sync(0xffffffffu, ne && c < cta));
+    }
+    const int subs = sp.subs();
+    float* pc = g.pieces + static_cast<size_t>(T) * g.max_pieces * 2 * kTileRows * B;
+    // gather the 16 x subs x B partials to lane 0, which publishes them (its
+    // own stores + a release increment: no fence by the other lanes)
+    float all[2][kTileRows][B];
+#pragma unroll
+    for (int sb = 0; sb < 2; ++sb)
+#pragma unroll
+        for (int r = 0; r < kTileRows; ++r)
+#pragma unroll
+            for (int b = 0; b < B; ++b) all[sb][r][b] = __shfl_sync(0xffffffffu, v[sb][b], r);
+    if (slot > 0) {
+        if (lane == 0) {
+            float4* dst = reinterpret_cast<float4*>(pc + static_cast<size_t>(slot) * 2 * kTileRows * B);
+            const float* src = &all[0][0][0];
+#pragma unroll
+            for (int q = 0; q < 2 * kTileRows * B / 4; ++q)
+                dst[q] = make_float4(src[4 * q], src[4 * q + 1], src[4 * q + 2], src[4 * q + 3]);
+            red_release_add(g.count + T, 1u);
+        }
+        return false;
+    }
+    // slot 0: wait for the np - 1 others, then sum in CTA order
+    if (lane == 0)
+        while (ld_acquire(g.count + T) < static_cast<unsigned>(np - 1)) {
+        }
+    __syncwarp();
+    fence_acq_rel_gpu();
+#pragma unroll
+    for (int sb = 0; sb < 2; ++sb)
 #pragma unroll
         for (int b = 0; b < B; ++b) {
-            acc[b] += __shfl_xor_sync(0xffffffffu, acc[b], 1);
-            if (h == 0) part[(lu * 16 + i) * B + b] = acc[b];
+            float acc = v[sb][b];
+            if (lane < kTileRows && sb < subs)
+                for (int q = 1; q < np; ++q) acc += __ldcg(pc + ((q * 2 + sb) * kTileRows + lane) * B + b);
+            v[sb][b] = acc;
         }
-    }
+    if (lane == 0) g.count[T] = 0u;
+    return true;
+}
+
+// Per-phase shared state of a GEMV phase (computed once, read by all warps).
+struct GemvShared {
+    MkSplit sp;
+    int ulo, uhi, Tf;
+    unsigned cnt[kMkMaxLocalTiles];  // chunk completions per local tile (0x10000 = tile complete)
+    float inv[4];
+    unsigned next;                   // dynamic chunk assignment
 };
 
-// ---------------------------------------------------------- piece write --
-// After the CTA's units are reduced into shared memory: for every output
-// tile the CTA touched, sum its units (in unit order) and store the piece in
-// the tile's slot = number of non-empty CTAs before this one on the tile.
-template <int ES, int B>
-__device__ void write_pieces(const MkGemv& g, const Geo<ES>& geo, const float* spart, int tid, int cta, int ncta,
-                             const float* inv) {
-    const int warp = tid >> 5, lane = tid & 31, i = lane & 15;
-    int j = 0;
-    for (int U = geo.cl; U < geo.ch; ++j) {
-        int a, e;
-        const int T = geo.out_tile(U, a, e);
-        const int lo = U, hi = min(e, geo.ch);
-        U = hi;
-        if ((j & (kWarpsMk - 1)) != warp) continue;
-        int slot = 0;
-        for (int c = unit_cta(a, geo.total, ncta); c < cta; ++c)
-            if (unit_lo(geo.total, c + 1, ncta) > unit_lo(geo.total, c, ncta)) ++slot;
-        if (lane < 16) {
-            float v[B];
-#pragma unroll
-            for (int b = 0; b < B; ++b) v[b] = 0.f;
-            for (int u = lo; u < hi; ++u)
-#pragma unroll
-                for (int b = 0; b < B; ++b) v[b] += spart[((u - geo.cl) * 16 + i) * B + b];
-            float* dst = g.out.base + (static_cast<size_t>(slot) * g.out.R + T * 16 + i) * B;
-#pragma unroll
-            for (int b = 0; b < B; ++b) dst[b] = v[b] * inv[b];
-        }
-    }
-}
-
-// ------------------------------------------------------------ GEMV phase --
 template <typename W, int B>
-__device__ __forceinline__ void gemv_phase(const MkPhase& ph, int phase_idx, Smem sm, int tid, int cta,
-                                           int ncta, Cursor<sizeof(W)>& cs, Cursor<sizeof(W)>& is,
-                                           Cursor<sizeof(W)>& pf, uint32_t& seq, uint64_t policy,
-                                           unsigned long long* tr) {
+__device__ void gemv_phase(const MkGemv& g, const Smem& sm, GemvShared& sh, int tid, int cta, int G, uint32_t& cseq,
+                           uint32_t& xphase, int stages, unsigned long long* tr, unsigned long long* ctr) {
     constexpr int ES = sizeof(W);
-    const MkGemv& g = ph.g;
-    // this phase's carve of the shared region: x planes (stride x_len), then unit partials
-    sm.x_cap = g.x_len;
-    sm.part = reinterpret_cast<float*>(static_cast<char*>(sm.x) +
-                                       ((static_cast<size_t>(B) * XPlanes<W>::kPlanes * g.x_len * ES + 15) & ~size_t(15)));
-    stage_x<W, B>(g, sm, tid, cta, ncta);
-    if (tr && tid == 0) tr[2] = gtimer();
+    const int warp = tid >> 5, lane = tid & 31;
+    // ---- stage the input planes (one bulk copy), split, RMSNorm scale ----
+    if (tid == 0) {
+        const uint32_t xbytes = static_cast<uint32_t>(B) * g.in.len * PlaneIO<W>::kBytesPerElem;
+        fence_proxy_async_global();
+        mbar_expect_tx(sm.xbar, xbytes);
+        bulk_g2s_plain(sm.x, g.in.p, xbytes, sm.xbar);
+        sh.sp.init(g.seg, g.nseg, g.dual, ES);
+        sh.ulo = sh.sp.lo(cta, G);
+        sh.uhi = sh.sp.lo(cta + 1, G);
+        sh.Tf = sh.ulo < sh.uhi ? sh.sp.tile_of(sh.ulo) : 0;
+        sh.next = 0u;
+    }
+    if (tid < kMkMaxLocalTiles) sh.cnt[tid] = 0u;
+    const int rec_per_tile = (g.rec_c0 + g.rec_c1) * kTileRows * B;
+    {
+        float4* r4 = reinterpret_cast<float4*>(sm.rec);
+        const int n4 = g.rec_ntl * rec_per_tile / 4;
+        for (int q = tid; q < n4; q += kConsumerThreads) r4[q] = make_float4(0.f, 0.f, 0.f, 0.f);
+    }
+    if (g.norm_src) {
+        float ss[B];
+#pragma unroll
+        for (int b = 0; b < B; ++b) {
+            ss[b] = 0.f;
+            for (int j = tid * 4; j < g.norm_len; j += kConsumerThreads * 4) {
+                const float4 x = __ldcg(reinterpret_cast<const float4*>(g.norm_src + static_cast<size_t>(b) * g.norm_ld + j));
+                ss[b] = fmaf(x.x, x.x, ss[b]);
+                ss[b] = fmaf(x.y, x.y, ss[b]);
+                ss[b] = fmaf(x.z, x.z, ss[b]);
+                ss[b] = fmaf(x.w, x.w, ss[b]);
+            }
+            ss[b] = warp_sum(ss[b]);
+        }
+        if (lane == 0)
+#pragma unroll
+            for (int b = 0; b < B; ++b) sm.misc[warp * 4 + b] = ss[b];
+        consumer_sync();
+        if (tid < B) {
+            float t = 0.f;
+            for (int w = 0; w < kConsumerWarps; ++w) t += sm.misc[w * 4 + tid];
+            sh.inv[tid] = 1.0f / sqrtf(t / static_cast<float>(g.norm_len) + g.eps);
+        }
+    } else if (tid < B) {
+        sh.inv[tid] = 1.f;
+    }
+    consumer_sync();
+    const MkSplit& sp = sh.sp;
     float inv[B];
 #pragma unroll
-    for (int b = 0; b < B; ++b) inv[b] = sm.misc[128 + b];
-    const int warp = tid >> 5, lane = tid & 31;
-    Geo<ES> geo;
-    geo.init(g, cta, ncta);
-    while (!cs.done() && cs.p == phase_idx) {
-        const uint32_t slot = seq % kSlots, par = (seq / kSlots) & 1u;
-        uint64_t* bar = sm.full + warp * kSlots + slot;
-        char* buf = sm.slots + (static_cast<size_t>(warp) * kSlots + slot) * kUnitBytes;
-        mbar_wait(bar, par);
-        const int kbase = g.seg[cs.s].x_off + cs.u * kUnitLines * (kLineBytes / ES);
-        UnitDot<W, B>::run(buf, cs.lines(), sm, kbase, lane, sm.part, cs.U - geo.cl);
+    for (int b = 0; b < B; ++b) inv[b] = sh.inv[b];
+    mbar_wait(sm.xbar, xphase & 1u);
+    ++xphase;
+    if (tr && tid == 0) tr[1] = gtimer();
+
+    // ---- chunks (boundary tiles first): chunk -> warp cseq % 8; the warp that
+    // completes a tile's last chunk finalizes the tile right away ----
+    const W* xs = static_cast<const W*>(sm.x);
+    const int c_stride[2] = {0, g.rec_c0};
+    ChunkSeq seq;
+    seq.begin(sp, sh.ulo, sh.uhi);
+    int T_prev = -1, c_tile = 0, pos = 0;
+    const uint32_t cbase = cseq;
+    for (;;) {
+        // grab the next chunk (dynamic: a warp held up by a tile exchange never stalls the ring)
+        int jn = 0;
+        if (lane == 0) jn = static_cast<int>(atomicAdd(&sh.next, 1u));
+        jn = __shfl_sync(0xffffffffu, jn, 0);
+        int nl = 0, s = 0, line = 0, T = 0, sub = 0, c = 0;
+        while (pos <= jn && !seq.done()) {  // walk to chunk jn (every chunk is visited once per warp)
+            nl = seq.it.lines(sp);
+            s = seq.it.s;
+            line = seq.it.line;
+            T = seq.tile(sp);
+            sub = seq.sub(sp);
+            c = seq.c_run;
+            c_tile = T == T_prev ? c_tile + 1 : 0;  // chunk index inside the output tile
+            T_prev = T;
+            seq.advance(sp, nl);
+            ++pos;
+        }
+        if (pos <= jn) break;  // past the last chunk
+        const uint32_t cs = cbase + static_cast<uint32_t>(jn);
+        const bool last_of_tile = seq.done() || seq.tile(sp) != T;
+        const int k = T - sh.Tf;
+        const uint32_t slot = cs % stages, par = (cs / stages) & 1u;
+        mbar_wait(&sm.full[slot], par);
+        const unsigned long long t_wait = ctr ? gtimer() : 0ull;
+        const int kbase = g.seg[s].x_off + line * (kLineBytes / ES);
+        float* rec = sm.rec + k * rec_per_tile + (c_stride[sub] + c) * kTileRows * B;
+        ChunkDot<W, B>::run(sm.ring + static_cast<size_t>(slot) * kChunkBytes, nl, xs, g.in.len, kbase, lane, rec);
         __syncwarp();
-        // refill this slot with the unit kSlots ahead (possibly in a later phase)
-        if (!is.done()) {
-            if (lane == 0) {
-                fence_proxy_async();
-                mbar_expect_tx(bar, static_cast<uint32_t>(is.bytes()));
-                bulk_g2s(buf, is.src(), static_cast<uint32_t>(is.bytes()), bar, policy);
+        if (ctr && lane == 0 && cs < 8192) {
+            ctr[cs * 4 + 1] = t_wait;
+            ctr[cs * 4 + 2] = gtimer();
+            ctr[cs * 4 + 3] = warp;
+        }
+        unsigned done = 0;
+        if (lane == 0) {
+            mbar_arrive(&sm.empty[slot]);
+            __threadfence_block();
+            // every chunk adds 1; the tile's last chunk adds 0x10000 - c_tile, so the
+            // counter reaches exactly 0x10000 when all of the tile's chunks are reduced
+            const unsigned add = last_of_tile ? 0x10000u - static_cast<unsigned>(c_tile) : 1u;
+            done = atomicAdd(&sh.cnt[k], add) + add == 0x10000u;
+        }
+        done = __shfl_sync(0xffffffffu, done, 0);
+        if (!done) continue;
+        __threadfence_block();
+        // ---- finalize tile T: sum its chunk records in chunk order ----
+        float v[2][B];
+        const float* rt = sm.rec + k * rec_per_tile;
+#pragma unroll
+        for (int sb = 0; sb < 2; ++sb)
+#pragma unroll
+            for (int b = 0; b < B; ++b) {
+                float acc = 0.f;
+                if (lane < kTileRows) {
+                    const int n = sb ? g.rec_c1 : g.rec_c0;
+                    for (int q = 0; q < n; ++q) acc += rt[((c_stride[sb] + q) * kTileRows + lane) * B + b];
+                }
+                v[sb][b] = acc;
             }
-            is.advance();
-        }
-        // keep HBM busy through the phase overheads: L2 prefetch further ahead
-        if (!pf.done()) {
-            if (lane == 0) prefetch_l2_bulk(pf.src(), static_cast<uint32_t>(pf.bytes()));
-            pf.advance();
-        }
-        ++seq;
-        cs.advance();
+        if (!exchange_pieces<B>(g, sp, T, cta, G, lane, v)) continue;
+        finalize_rows<W, B>(g, sp, T, lane, v, inv);
     }
-    if (tr && lane == 0) tr[4 + (warp & 1)] = gtimer();  // units done: warps 0 and 1
-    __syncthreads();
-    if (tr && tid == 0) tr[6] = gtimer();
-    write_pieces<ES, B>(g, geo, sm.part, tid, cta, ncta, inv);
-    if (tr && tid == 0) tr[7] = gtimer();
+    cseq = cbase + static_cast<uint32_t>(pos);  // every warp walked all chunks of the phase
+    consumer_sync();
+    if (tr && tid == 0) tr[3] = gtimer();
 }
 
-// ---------------------------------------------------------- argmax phase --
-// logits = sum of the head pieces; per-CTA best (ties -> lowest index,
-// math.hpp:132-140); the last CTA (ticket) reduces the CTA bests in CTA order,
-// sets the next input token and advances the length register.
-template <int B>
-__device__ void argmax_phase(const MkArgmax& m, const Smem& sm, int tid, int cta, int ncta) {
+// ----------------------------------------------------------- attention ----
+template <typename T, int PER>
+__device__ __forceinline__ void load_kv_row(const T* p, float* out) {
+    if constexpr (sizeof(T) == 2 && PER == 4) {
+        const uint2 v = __ldcg(reinterpret_cast<const uint2*>(p));
+        out[0] = bf16lo(v.x);
+        out[1] = bf16hi(v.x);
+        out[2] = bf16lo(v.y);
+        out[3] = bf16hi(v.y);
+    } else if constexpr (sizeof(T) == 4 && PER == 4) {
+        const float4 v = __ldcg(reinterpret_cast<const float4*>(p));
+        out[0] = v.x;
+        out[1] = v.y;
+        out[2] = v.z;
+        out[3] = v.w;
+    } else {
+#pragma unroll
+        for (int e = 0; e < PER; ++e) out[e] = to_f32<T>(p[e]);
+    }
+}
+
+template <typename W, int B, int DH>
+__device__ void attn_phase(const MkAttn& a, const Smem& sm, int tid, int cta, int G) {
+    constexpr int PER = DH / 32, KU = 8, ST = DH + 2;
     const int warp = tid >> 5, lane = tid & 31;
-    const int r0 = unit_lo(m.vocab, cta, ncta), r1 = unit_lo(m.vocab, cta + 1, ncta);
-    float* sv = sm.misc;                                       // [warps][B]
-    int* si = reinterpret_cast<int*>(sm.misc + kWarpsMk * 4);  // [warps][B]
+    const int pos = *a.pos, len = pos + 1;
+    RowSplit rs{B * a.n_heads * len};
+    const int r0 = rs.lo(cta, G), r1 = rs.lo(cta + 1, G);
+    float* wst = sm.rec;  // [warps][DH + 2]: acc, l, m
+    for (int bh = r0 / len; bh * len < r1; ++bh) {
+        const int lo_bh = bh * len, hi_bh = lo_bh + len;
+        const int j0 = static_cast<int>((r0 > lo_bh ? r0 : lo_bh) - lo_bh);
+        const int j1 = static_cast<int>((r1 < hi_bh ? r1 : hi_bh) - lo_bh);
+        if (j1 <= j0) continue;
+        const int b = bh / a.n_heads, h = bh % a.n_heads;
+        const W* Kc = static_cast<const W*>(a.kcache) + b * a.cache_bstride + h * a.cache_hstride;
+        const W* Vc = static_cast<const W*>(a.vcache) + b * a.cache_bstride + h * a.cache_hstride;
+        float qr[PER];
+        {
+            const float* q = a.qbuf + static_cast<size_t>(b) * a.q_ld + h * DH + lane * PER;
+#pragma unroll
+            for (int e = 0; e < PER; ++e) qr[e] = __ldcg(q + e) * a.scale;
+        }
+        // this warp's keys
+        const int n = j1 - j0;
+        const int k0 = j0 + n * warp / kConsumerWarps, k1 = j0 + n * (warp + 1) / kConsumerWarps;
+        float m = -CUDART_INF_F, l = 0.f, acc[PER];
+#pragma unroll
+        for (int e = 0; e < PER; ++e) acc[e] = 0.f;
+        for (int kb = k0; kb < k1; kb += KU) {
+            float kr[KU][PER], vr[KU][PER];
+#pragma unroll
+            for (int u = 0; u < KU; ++u) {
+                const int jj = min(kb + u, k1 - 1);  // clamp: duplicate loads are masked below
+                load_kv_row<W, PER>(Kc + static_cast<long long>(jj) * DH + lane * PER, kr[u]);
+                load_kv_row<W, PER>(Vc + static_cast<long long>(jj) * DH + lane * PER, vr[u]);
+            }
+            float sc[KU];
+            float mb = -CUDART_INF_F;
+#pragma unroll
+            for (int u = 0; u < KU; ++u) {
+                float d = 0.f;
+#pragma unroll
+                for (int e = 0; e < PER; ++e) d = fmaf(qr[e], kr[u][e], d);
+                d = warp_sum(d);
+                sc[u] = kb + u < k1 ? d : -CUDART_INF_F;
+                mb = fmaxf(mb, sc[u]);
+            }
+            const float mn = fmaxf(m, mb);
+            const float r = expf(m - mn);  // exp(-inf) = 0 on the first round
+            l *= r;
+#pragma unroll
+            for (int e = 0; e < PER; ++e) acc[e] *= r;
+#pragma unroll
+            for (int u = 0; u < KU; ++u) {
+                const float w = expf(sc[u] - mn);
+                l += w;
+#pragma unroll
+                for (int e = 0; e < PER; ++e) acc[e] = fmaf(w, vr[u][e], acc[e]);
+            }
+            m = mn;
+        }
+#pragma unroll
+        for (int e = 0; e < PER; ++e) wst[warp * ST + lane * PER + e] = acc[e];
+        if (lane == 0) {
+            wst[warp * ST + DH] = l;
+            wst[warp * ST + DH + 1] = m;
+        }
+        consumer_sync();
+        // CTA partial (warps merged in order) -> pieces or direct
+        const int c0 = rs.cta_of(lo_bh, G), c1 = rs.cta_of(hi_bh - 1, G);
+        const int np = rs.nonempty(c0, c1 + 1, G);
+        float M = -CUDART_INF_F;
+        for (int w = 0; w < kConsumerWarps; ++w) M = fmaxf(M, wst[w * ST + DH + 1]);
+        float* part = a.partial + static_cast<long long>(bh) * a.splits * ST;
+        if (np > 1) {
+            const int slot = rs.nonempty(c0, cta, G);
+            for (int e = tid; e < DH + 1; e += kConsumerThreads) {
+                float t = 0.f;
+                for (int w = 0; w < kConsumerWarps; ++w) {
+                    const float mw = wst[w * ST + DH + 1];
+                    if (mw != -CUDART_INF_F) t += wst[w * ST + e] * expf(mw - M);
+                }
+                part[slot * ST + e] = t;
+            }
+            if (tid == 0) part[slot * ST + DH + 1] = M;
+            fence_acq_rel_gpu();
+            consumer_sync();
+            if (tid == 0) sm.misc[64] = atom_add_acq_rel(a.count + bh, 1u) == static_cast<unsigned>(np - 1) ? 1.f : 0.f;
+            consumer_sync();
+            if (sm.misc[64] != 0.f) {
+                fence_acq_rel_gpu();
+                float MM = -CUDART_INF_F;
+                for (int q = 0; q < np; ++q) MM = fmaxf(MM, __ldcg(part + q * ST + DH + 1));
+                float L = 0.f;
+                for (int q = 0; q < np; ++q) L += __ldcg(part + q * ST + DH) * expf(__ldcg(part + q * ST + DH + 1) - MM);
+                const float invL = 1.0f / L;
+                for (int e = tid; e < DH; e += kConsumerThreads) {
+                    float o = 0.f;
+                    for (int q = 0; q < np; ++q) o = fmaf(__ldcg(part + q * ST + e), expf(__ldcg(part + q * ST + DH + 1) - MM), o);
+                    PlaneIO<W>::put(a.out, b, h * DH + e, o * invL);
+                }
+                if (tid == 0) a.count[bh] = 0u;
+            }
+        } else {
+            float L = 0.f;
+            for (int w = 0; w < kConsumerWarps; ++w) {
+                const float mw = wst[w * ST + DH + 1];
+                if (mw != -CUDART_INF_F) L += wst[w * ST + DH] * expf(mw - M);
+            }
+            const float invL = 1.0f / L;
+            for (int e = tid; e < DH; e += kConsumerThreads) {
+                float t = 0.f;
+                for (int w = 0; w < kConsumerWarps; ++w) {
+                    const float mw = wst[w * ST + DH + 1];
+                    if (mw != -CUDART_INF_F) t += wst[w * ST + e] * expf(mw - M);
+                }
+                PlaneIO<W>::put(a.out, b, h * DH + e, t * invL);
+            }
+        }
+        consumer_sync();
+    }
+}
+
+// ------------------------------------------------------- argmax / vec ----
+template <int B>
+__device__ void argmax_phase(const MkArgmax& m, const Smem& sm, int tid, int cta) {
+    if (cta != 0) return;
+    const int warp = tid >> 5, lane = tid & 31;
+    float* sv = sm.misc;
+    int* si = reinterpret_cast<int*>(sm.misc + 64);
     for (int b = 0; b < B; ++b) {
         float bv = -CUDART_INF_F;
         int bi = 0x7fffffff;
-        for (int r = r0 + tid; r < r1; r += kThreadsMk) {
-            const float v = piece_sum<B>(m.pc, r, b);
-            m.logits[static_cast<long long>(b) * m.vocab + r] = v;
-            if (better(v, r, bv, bi)) {
+        for (int t = tid; t < m.ntiles; t += kConsumerThreads) {
+            const float v = __ldcg(m.cand_v + t * B + b);
+            const int i = __ldcg(m.cand_i + t * B + b);
+            if (better(v, i, bv, bi)) {
                 bv = v;
-                bi = r;
+                bi = i;
             }
         }
 #pragma unroll
@@ -374,138 +530,159 @@ __device__ void argmax_phase(const MkArgmax& m, const Smem& sm, int tid, int cta
             si[warp * 4 + b] = bi;
         }
     }
-    __syncthreads();
-    __shared__ unsigned last;
+    consumer_sync();
     if (tid == 0) {
+        const int step = m.step ? *m.step : 0;
         for (int b = 0; b < B; ++b) {
             float bv = -CUDART_INF_F;
             int bi = 0x7fffffff;
-            for (int w = 0; w < kWarpsMk; ++w)
+            for (int w = 0; w < kConsumerWarps; ++w)
                 if (better(sv[w * 4 + b], si[w * 4 + b], bv, bi)) {
                     bv = sv[w * 4 + b];
                     bi = si[w * 4 + b];
                 }
-            m.best_v[cta * B + b] = bv;
-            m.best_i[cta * B + b] = bi;
-        }
-        __threadfence();
-        last = atomicAdd(m.ticket, 1u) + 1u == static_cast<unsigned>(ncta);
-        if (last) __threadfence();
-    }
-    __syncthreads();
-    if (!last || warp != 0) return;
-    for (int b = 0; b < B; ++b) {
-        float bv = -CUDART_INF_F;
-        int bi = 0x7fffffff;
-        for (int c = lane; c < ncta; c += 32) {
-            const float v = __ldcg(m.best_v + c * B + b);
-            const int i = __ldcg(m.best_i + c * B + b);
-            if (better(v, i, bv, bi)) {
-                bv = v;
-                bi = i;
-            }
-        }
-#pragma unroll
-        for (int o = 16; o > 0; o >>= 1) {
-            const float ov = __shfl_xor_sync(0xffffffffu, bv, o);
-            const int oi = __shfl_xor_sync(0xffffffffu, bi, o);
-            if (better(ov, oi, bv, bi)) {
-                bv = ov;
-                bi = oi;
-            }
-        }
-        if (lane == 0) {
             if (bi == 0x7fffffff) bi = 0;
             m.tokens[b] = bi;
-            if (m.out) m.out[static_cast<long long>(b) * m.out_ld + *m.step] = bi;
+            if (m.out) m.out[static_cast<long long>(b) * m.out_ld + step] = bi;
         }
-    }
-    if (lane == 0) {
         *m.pos += m.pos_inc;
-        *m.step += 1;
-        *m.ticket = 0u;
+        if (m.step) *m.step = step + 1;
+    }
+}
+
+template <typename W, int B>
+__device__ void vec_phase(const MkVec& v, int tid, int cta, int G) {
+    const int i0 = static_cast<int>(static_cast<long long>(v.len) * cta / G);
+    const int i1 = static_cast<int>(static_cast<long long>(v.len) * (cta + 1) / G);
+#pragma unroll
+    for (int b = 0; b < B; ++b) {
+        const W* er = v.emb ? static_cast<const W*>(v.emb) + static_cast<long long>(__ldcg(v.tokens + b)) * v.emb_ld
+                            : nullptr;
+        for (int i = i0 + tid; i < i1; i += kConsumerThreads) {
+            const float x = er ? to_f32<W>(er[i]) : __ldcg(v.src + static_cast<size_t>(b) * v.src_ld + i);
+            if (v.xres) v.xres[static_cast<size_t>(b) * v.xres_ld + i] = x;
+            PlaneIO<W>::put(v.out, b, i, x * v.gamma[i]);
+        }
     }
 }
 
 // ----------------------------------------------------------- the kernel --
 template <typename W, int B, int DH>
-__global__ void __launch_bounds__(kThreadsMk, 1) decode_mk_kernel(const MkPhase* __restrict__ phases, int p_begin,
-                                                                  int p_end, unsigned* bar, int region_bytes,
-                                                                  int red_floats, unsigned long long* trace) {
-    extern __shared__ __align__(128) uint8_t smem_raw[];
-    constexpr int ES = sizeof(W);
+__global__ void __launch_bounds__(kThreads, 1) decode_mk_kernel(const __grid_constant__ MkLaunch L) {
+    extern __shared__ __align__(1024) uint8_t smem_raw[];
     Smem sm;
-    sm.slots = reinterpret_cast<char*>(smem_raw);
-    sm.full = reinterpret_cast<uint64_t*>(smem_raw + static_cast<size_t>(kWarpsMk) * kSlots * kUnitBytes);
-    sm.x = sm.full + kWarpsMk * kSlots;
-    sm.x_cap = 0;
-    sm.part = nullptr;  // carved per phase (gemv_phase)
-    sm.red = reinterpret_cast<float*>(static_cast<char*>(sm.x) + region_bytes);
-    sm.misc = sm.red + red_floats;
+    sm.ring = reinterpret_cast<char*>(smem_raw);
+    sm.full = reinterpret_cast<uint64_t*>(smem_raw + static_cast<size_t>(L.stages) * kChunkBytes);
+    sm.empty = sm.full + L.stages;
+    sm.xbar = sm.empty + L.stages;
+    sm.x = reinterpret_cast<char*>(sm.full) + mk_barrier_bytes(L.stages);
+    sm.rec = reinterpret_cast<float*>(static_cast<char*>(sm.x) + L.x_bytes);
+    const int rec_floats = std::max(L.rec_chunks * kTileRows * B, kConsumerWarps * (DH + 2));
+    sm.misc = sm.rec + rec_floats;
+    sm.desc = reinterpret_cast<MkPhase*>(sm.misc + 256);
+    sm.dbar = reinterpret_cast<uint64_t*>(sm.desc + 2);
+    sm.gsh = sm.dbar + 2;
 
-    const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31, cta = blockIdx.x, ncta = gridDim.x;
-    if (tid < kWarpsMk * kSlots) mbar_init(&sm.full[tid], 1);
-    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31, cta = blockIdx.x, G = gridDim.x;
+    if (tid == 0) {
+        for (int i = 0; i < L.stages; ++i) {
+            mbar_init(&sm.full[i], 1);
+            mbar_init(&sm.empty[i], 1);
+        }
+        mbar_init(sm.xbar, 1);
+        mbar_init(&sm.dbar[0], 1);
+        mbar_init(&sm.dbar[1], 1);
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
     __syncthreads();
 
-    // per-warp unit streams: compute (cs), bulk-copy issue (is, kSlots ahead), L2 prefetch (pf)
-    Cursor<ES> cs, is, pf;
-    cs.init(phases, p_begin, p_end, cta, ncta, warp);
-    is.init(phases, p_begin, p_end, cta, ncta, warp);
-    pf.init(phases, p_begin, p_end, cta, ncta, warp);
-    const uint64_t policy = evict_first_policy();
-    uint32_t seq = 0;
-    for (int sl = 0; sl < kSlots && !is.done(); ++sl) {
-        if (lane == 0) {
-            uint64_t* b = sm.full + warp * kSlots + sl;
-            mbar_expect_tx(b, static_cast<uint32_t>(is.bytes()));
-            bulk_g2s(sm.slots + (static_cast<size_t>(warp) * kSlots + sl) * kUnitBytes, is.src(),
-                     static_cast<uint32_t>(is.bytes()), b, policy);
+    if (warp == kConsumerWarps) {
+        // ================= producer: weight stream of every GEMV phase =================
+        if (lane != 0) return;
+        constexpr int ES = sizeof(W);
+        const uint64_t policy = evict_first_policy();
+        uint32_t seq = 0;
+        for (int p = L.p_begin; p < L.p_end; ++p) {
+            const MkPhase& ph = L.phases[p];
+            if (ph.kind != kMkGemv) continue;
+            unsigned long long* tr =
+                L.trace ? L.trace + (static_cast<size_t>(cta) * (L.p_end - L.p_begin) + (p - L.p_begin)) * 16 : nullptr;
+            bool first = true;
+            const MkGemv& g = ph.g;
+            MkSplit sp;
+            sp.init(g.seg, g.nseg, g.dual, ES);
+            const char* wbase[3];
+            size_t tbytes[3];
+            for (int q = 0; q < 3; ++q) {
+                wbase[q] = static_cast<const char*>(g.seg[q].w);
+                tbytes[q] = g.seg[q].layout(ES).tile_bytes();
+            }
+            ChunkSeq cs;
+            cs.begin(sp, sp.lo(cta, G), sp.lo(cta + 1, G));
+            for (; !cs.done(); ++seq) {
+                const int nl = cs.it.lines(sp);
+                const uint32_t bytes = static_cast<uint32_t>(nl) * kLineTileBytes;
+                const char* src = wbase[cs.it.s] + static_cast<size_t>(cs.it.t) * tbytes[cs.it.s] +
+                                  static_cast<size_t>(cs.it.line) * kLineTileBytes;
+                cs.advance(sp, nl);
+                const uint32_t slot = seq % L.stages;
+                mbar_wait(&sm.empty[slot], ((seq / L.stages) & 1u) ^ 1u);
+                mbar_expect_tx(&sm.full[slot], bytes);
+                bulk_g2s(sm.ring + static_cast<size_t>(slot) * kChunkBytes, src, bytes, &sm.full[slot], policy);
+                if (tr) {
+                    if (cta == 0 && seq < 8192) L.trace[static_cast<size_t>(G) * (L.p_end - L.p_begin) * 16 + seq * 4] = gtimer();
+                    if (first) tr[5] = gtimer();
+                    tr[6] = gtimer();
+                    first = false;
+                }
+            }
         }
-        is.advance();
-    }
-    for (int k = 0; k < kSlots + kPrefetch && !pf.done(); ++k) {
-        if (k >= kSlots && lane == 0) prefetch_l2_bulk(pf.src(), static_cast<uint32_t>(pf.bytes()));
-        pf.advance();
+        return;
     }
 
-    const int nph = p_end - p_begin;
-    for (int p = p_begin; p < p_end; ++p) {
-        const int idx = p - p_begin;
-        unsigned long long* tr = trace ? trace + (static_cast<size_t>(cta) * nph + idx) * 8 : nullptr;
-        if (tr && tid == 0) tr[0] = gtimer();
-        const MkPhase& ph = phases[p];
-        // the history of the coming attention is immutable: prefetch it to L2
-        if (ph.kind == kMkGemv && p + 2 < p_end && phases[p + 2].kind == kMkAttn && phases[p + 1].kind == kMkGemv)
-            attn_prefetch<W, B, DH>(phases[p + 2].a, tid, cta, ncta);
-        if (idx > 0) {  // grid barrier: all CTAs finished phase idx-1
+    // ================= consumers =================
+    constexpr uint32_t kDescBytes = sizeof(MkPhase);
+    if (tid == 0) {  // descriptor of the first phase
+        mbar_expect_tx(&sm.dbar[0], kDescBytes);
+        bulk_g2s_plain(&sm.desc[0], &L.phases[L.p_begin], kDescBytes, &sm.dbar[0]);
+    }
+    GemvShared& gsh = *static_cast<GemvShared*>(sm.gsh);
+    uint32_t cseq = 0, xphase = 0;
+    const int nph = L.p_end - L.p_begin;
+    for (int p = L.p_begin; p < L.p_end; ++p) {
+        const int idx = p - L.p_begin, buf = idx & 1;
+        unsigned long long* tr = L.trace ? L.trace + (static_cast<size_t>(cta) * nph + idx) * 16 : nullptr;
+        if (idx > 0) {  // grid barrier: every CTA finished phase idx-1
             if (tid == 0) {
-                const unsigned target = static_cast<unsigned>(idx) * ncta;
-                while (ld_acquire(bar) < target) __nanosleep(20);
+                const unsigned target = static_cast<unsigned>(idx) * G;
+                while (ld_acquire(L.bar) < target) {
+                }
             }
-            __syncthreads();
+            consumer_sync();
         }
-        if (tr && tid == 0) tr[1] = tr[2] = tr[4] = tr[5] = tr[6] = tr[7] = gtimer();
+        if (tid == 0 && p + 1 < L.p_end) {  // prefetch the next descriptor (its buffer's readers are done)
+            asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+            mbar_expect_tx(&sm.dbar[buf ^ 1], kDescBytes);
+            bulk_g2s_plain(&sm.desc[buf ^ 1], &L.phases[p + 1], kDescBytes, &sm.dbar[buf ^ 1]);
+        }
+        if (tr && tid == 0) for (int q = 0; q < 16; ++q) if (q != 5 && q != 6) tr[q] = gtimer();
+        mbar_wait(&sm.dbar[buf], (idx >> 1) & 1u);
+        const MkPhase& ph = sm.desc[buf];
         switch (ph.kind) {
-            case kMkGemv:
-                gemv_phase<W, B>(ph, p, sm, tid, cta, ncta, cs, is, pf, seq, policy, tr);
-                break;
-            case kMkAttn:
-                attn_phase<W, B, DH>(ph.a, sm, tid, cta, ncta);
-                break;
-            case kMkArgmax:
-                argmax_phase<B>(ph.m, sm, tid, cta, ncta);
-                break;
-            default:
-                break;
+            case kMkGemv: gemv_phase<W, B>(ph.g, sm, gsh, tid, cta, G, cseq, xphase, L.stages, tr, tr && cta == 0 ? L.trace + static_cast<size_t>(G) * nph * 16 : nullptr); break;
+            case kMkAttn: attn_phase<W, B, DH>(ph.a, sm, tid, cta, G); break;
+            case kMkArgmax: argmax_phase<B>(ph.m, sm, tid, cta); break;
+            default: vec_phase<W, B>(ph.v, tid, cta, G); break;
         }
-        // arrive: this CTA's writes of phase idx are complete
-        __syncthreads();
-        if (tr && tid == 0) tr[3] = gtimer();
-        if (tid == 0) {
-            __threadfence();
-            const unsigned v = atomicAdd(bar, 1u) + 1u;
-            if (v == static_cast<unsigned>(nph) * ncta) *bar = 0u;  // last arrival of the launch: reset
+        consumer_sync();
+        if (tr && tid == 0) tr[4] = gtimer();
+        if (tid == 0) {  // arrive (release): this CTA's writes of phase idx are complete
+            if (idx + 1 < nph) {
+                red_release_add(L.bar, 1u);  // fire and forget
+            } else {
+                const unsigned v = atom_add_acq_rel(L.bar, 1u) + 1u;
+                if (v == static_cast<unsigned>(nph) * G) *L.bar = 0u;  // last arrival of the launch: reset
+            }
         }
     }
 }
@@ -516,7 +693,7 @@ void launch_t(const MkLaunch& L, cudaStream_t s) {
     cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, L.smem_bytes);
     cudaLaunchConfig_t cfg{};
     cfg.gridDim = dim3(L.grid);
-    cfg.blockDim = dim3(kThreadsMk);
+    cfg.blockDim = dim3(kThreads);
     cfg.dynamicSmemBytes = L.smem_bytes;
     cfg.stream = s;
     cudaLaunchAttribute attr[1];
@@ -524,90 +701,69 @@ void launch_t(const MkLaunch& L, cudaStream_t s) {
     attr[0].val.cooperative = 1;
     cfg.attrs = attr;
     cfg.numAttrs = 1;
-    cudaLaunchKernelEx(&cfg, fn, L.phases, L.p_begin, L.p_end, L.bar, L.region_bytes, L.red_floats, L.trace);
+    cudaLaunchKernelEx(&cfg, fn, L);
 }
 
 }  // namespace mk
 
 // --------------------------------------------------------- host mirrors --
-namespace {
-struct HostSeg {
-    int ntiles, nunits;
-};
-HostSeg host_seg(const GemvSeg& s, int es) {
-    const WLayout l = s.layout(es);
-    return {l.ntiles(), l.nunits()};
-}
-long long ulo(long long total, int c, int G) { return total * c / G; }
-}  // namespace
-
 int mk_units(const GemvSeg* seg, int nseg, int dual, int esize) {
-    if (dual) {
-        const HostSeg a = host_seg(seg[0], esize), b = host_seg(seg[1], esize);
-        return a.ntiles * (a.nunits + b.nunits);
-    }
-    int t = 0;
-    for (int s = 0; s < nseg; ++s) {
-        const HostSeg h = host_seg(seg[s], esize);
-        t += h.ntiles * h.nunits;
-    }
-    return t;
+    MkSplit sp;
+    sp.init(seg, nseg, dual, esize);
+    return sp.total;
 }
 
 int mk_out_tiles(const GemvSeg* seg, int nseg, int dual, int esize) {
-    if (dual) return 2 * host_seg(seg[0], esize).ntiles;
-    int t = 0;
-    for (int s = 0; s < nseg; ++s) t += host_seg(seg[s], esize).ntiles;
-    return t;
+    MkSplit sp;
+    sp.init(seg, nseg, dual, esize);
+    return sp.out_tiles;
 }
 
-int mk_npieces(const GemvSeg* seg, int nseg, int dual, int esize, int grid, uint8_t* npieces) {
-    const long long total = mk_units(seg, nseg, dual, esize);
-    // unit ranges of the output tiles, in output-tile order
-    std::vector<std::pair<long long, long long>> rng;
+void mk_split_stats(const GemvSeg* seg, int nseg, int dual, int esize, int grid, int* max_pieces, int* rec_ntl,
+                    int* rec_c0, int* rec_c1) {
+    MkSplit sp;
+    sp.init(seg, nseg, dual, esize);
+    int mp = 1;
+    for (int T = 0; T < sp.out_tiles; ++T) {
+        int a, e;
+        sp.tile_span(T, a, e);
+        mp = std::max(mp, sp.nonempty(sp.cta_of(a, grid), sp.cta_of(e - 1, grid) + 1, grid));
+    }
+    int ntl = 1;
+    for (int c = 0; c < grid; ++c) {
+        const int ulo = sp.lo(c, grid), uhi = sp.lo(c + 1, grid);
+        if (ulo < uhi) ntl = std::max(ntl, sp.tile_of(uhi - 1) - sp.tile_of(ulo) + 1);
+    }
+    int c0 = 0, c1 = 0;
     if (dual) {
-        const HostSeg a = host_seg(seg[0], esize), b = host_seg(seg[1], esize);
-        const long long per = a.nunits + b.nunits;
-        for (int t = 0; t < a.ntiles; ++t) rng.push_back({t * per, t * per + a.nunits});
-        for (int t = 0; t < a.ntiles; ++t) rng.push_back({t * per + a.nunits, (t + 1) * per});
+        c0 = (sp.nlines[0] + kChunkLines - 1) / kChunkLines;
+        c1 = (sp.nlines[1] + kChunkLines - 1) / kChunkLines;
     } else {
-        long long ub = 0;
-        for (int s = 0; s < nseg; ++s) {
-            const HostSeg h = host_seg(seg[s], esize);
-            for (int t = 0; t < h.ntiles; ++t) rng.push_back({ub + t * h.nunits, ub + (t + 1) * h.nunits});
-            ub += static_cast<long long>(h.ntiles) * h.nunits;
-        }
+        for (int s = 0; s < nseg; ++s) c0 = std::max(c0, (sp.nlines[s] + kChunkLines - 1) / kChunkLines);
     }
-    int mx = 0;
-    for (size_t T = 0; T < rng.size(); ++T) {
-        int n = 0;
-        for (int c = 0; c < grid; ++c) {
-            const long long lo = std::max(ulo(total, c, grid), rng[T].first);
-            const long long hi = std::min(ulo(total, c + 1, grid), rng[T].second);
-            if (lo < hi) ++n;
-        }
-        if (n > 255) throw std::runtime_error("decode megakernel: more than 255 pieces on one tile");
-        npieces[T] = static_cast<uint8_t>(n);
-        mx = std::max(mx, n);
-    }
-    return mx;
+    *max_pieces = mp;
+    *rec_ntl = ntl;
+    *rec_c0 = c0;
+    *rec_c1 = c1;
 }
 
-int mk_region_bytes(int batch, WType wt, int x_len, int units_per_cta) {
-    const int es = wt == kBF16 ? 2 : 4, planes = wt == kBF16 ? 2 : 1;
-    return ((batch * planes * x_len * es + 15) & ~15) + units_per_cta * 16 * batch * 4;
+static int rec_floats(int rec_chunks, int batch, int d_head) {
+    return std::max(rec_chunks * kTileRows * batch, mk::kConsumerWarps * (d_head + 2));
 }
 
-int mk_red_floats(int batch, int n_heads, int d_head) {
-    return (std::max(mk::kWarpsMk * (d_head + 2), 3 * batch * n_heads) + 31) / 32 * 32;
+int mk_smem_bytes(int stages, int x_bytes, int rec_chunks, int batch, int d_head) {
+    return stages * kChunkBytes + mk::mk_barrier_bytes(stages) + x_bytes + rec_floats(rec_chunks, batch, d_head) * 4 +
+           256 * 4 + 2 * static_cast<int>(sizeof(MkPhase)) + 16 + static_cast<int>(sizeof(mk::GemvShared)) + 16;
 }
 
-int mk_smem_bytes(int region_bytes, int red_floats) {
-    return mk::kWarpsMk * mk::kSlots * kUnitBytes + mk::kWarpsMk * mk::kSlots * 8 + region_bytes + red_floats * 4 +
-           256 * 4 + 128;
+int mk_max_stages(int x_bytes, int rec_chunks, int batch, int d_head) {
+    const int budget = 227 * 1024 - 1024;  // dynamic shared memory per CTA (+ static / alignment slack)
+    int s = (budget - mk_smem_bytes(0, x_bytes, rec_chunks, batch, d_head)) / kChunkBytes;
+    while (s > 0 && mk_smem_bytes(s, x_bytes, rec_chunks, batch, d_head) > budget) --s;
+    return s;
 }
 
-int mk_warps() { return mk::kWarpsMk; }
+int mk_consumer_warps() { return mk::kConsumerWarps; }
 
 bool mk_launch(WType wt, int batch, int d_head, const MkLaunch& L, cudaStream_t s) {
 #define FSVD_MK(W, BB, DHH) \

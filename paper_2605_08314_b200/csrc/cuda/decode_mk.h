@@ -1,134 +1,155 @@
 // Phase program of the persistent decode megakernel (decode_mk.cu).
 //
-// Only the grid barrier synchronizes CTAs: a GEMV phase writes per-CTA
-// partial sums ("pieces") of its output rows, and the consuming phase's
-// input staging sums the pieces in CTA order and applies the producer's
-// epilogue (residual add, SiLU.mul, RoPE + KV append, attention merge).
+// A decode step is a list of phases separated by grid barriers. Each CTA has
+// one producer warp that streams the weight tiles of every GEMV phase of the
+// launch, in order, through a shared-memory ring (cp.async.bulk), never
+// waiting for activations; the consumer warps stage a phase's input vector
+// (one bulk copy of a ready-made "planes" buffer), reduce the ring's chunks
+// on the tensor cores, and finalize the phase's outputs.
+//
+// Output exchange: a CTA owns a contiguous range of (16-row tile, 128-byte
+// line) units. An output tile covered by one CTA is finalized by that CTA; a
+// tile shared by several CTAs is finalized by the last of them to arrive (a
+// per-tile counter), which sums the per-CTA partials ("pieces") in CTA order
+// -- deterministic bits for any launch structure (eager / per layer / full
+// step are bitwise identical). Finalizing applies the epilogue
+// once per row: RoPE + KV append, residual add + next RMSNorm's gamma,
+// SiLU.mul, logits, and writes the next phase's input planes.
 #pragma once
 
 #include "kernels.h"
 
 namespace fsvd::k {
 
-enum MkKind : int { kMkGemv = 0, kMkAttn = 1, kMkArgmax = 2 };
+enum MkKind : int { kMkGemv = 0, kMkAttn = 1, kMkArgmax = 2, kMkVec = 3 };
 
-// Pieces of a producer phase, slot-plane major: output row r (segment tiles
-// concatenated, 16 rows each), CTA slot j < S, batch b at base[(j*R + r)*B + b].
-// Every phase owns its buffer and a tile's unused slots stay zero (never
-// written), so a consumer sums all S planes without knowing the piece count.
-struct Pieces {
-    float* base;
-    int R;  // rows (output tiles * 16)
-    int S;  // slots (max pieces on any tile)
+// An activation vector in the form the GEMV consumes as its B operand:
+// bf16 weights: [B][2][len] bf16 (x = hi + lo, both RNE: fp32-grade
+// activations on bf16 tensor cores); fp32 weights: [B][len] fp32.
+// len is a multiple of 64 elements, padding stays zero.
+struct Planes {
+    void* p;
+    int len;
 };
 
-// One output segment of a producer, as seen by a consumer's input vector:
-// x[x_off + r] for r < rows comes from tile tbase + r/16, row r%16 of pc.
-struct InSeg {
-    int x_off, rows, tbase;
-    Pieces pc;
-};
-
-enum InKind : int {
-    kInPlain = 0,     // x = src
-    kInPieces = 1,    // x = sum(pieces) over the segments
-    kInResidual = 2,  // x = src + sum(pieces of seg[0]) (nseg 0: x = src); written back to dst
-    kInSilu = 3,      // x[r] = silu(sum gate) * sum(up), up = seg[0], gate = seg[1]
-    kInAttn = 4,      // x = merged attention partials (all heads)
-    kInEmbed = 5,     // x = E[tokens[b]] (weight dtype); written back to dst
-};
-
-struct AttnMerge {
-    const float* partial;  // [B*H][splits][d_head + 4] (acc, l, m)
-    int n_heads, d_head, splits;
-    const int* pos;        // attended positions 0 .. *pos
-};
-
-struct InputSpec {
-    int kind;
-    const float* src;  // [B][src_ld]
-    int src_ld;
-    float* dst;        // kInResidual write-back [B][dst_ld] (each CTA writes its slice)
-    int dst_ld;
-    int len;           // logical length of src/dst (kInResidual, kInPlain, kInEmbed)
-    const void* emb;   // kInEmbed: [V][emb_ld] weight dtype
-    int emb_ld;
-    const int* tokens; // kInEmbed: [B]
-    InSeg seg[3];
-    int nseg;
-    AttnMerge am;
+enum MkOut : int {
+    kOutPlanes = 0,  // out.p[x_off[s] + r] = v                       (rank spaces)
+    kOutResid = 1,   // xres[r] += v; out = xres[r] * gamma[r]         (o / down B)
+    kOutQKV = 2,     // q: RoPE -> qbuf; k: RoPE -> K cache[pos]; v -> V cache[pos]
+    kOutSilu = 3,    // dual: out = silu(gate) * up                     (up/gate B)
+    kOutLogits = 4,  // logits[b][r] = v, per-tile best -> cand        (head)
 };
 
 struct MkGemv {
-    GemvSeg seg[3];      // weights (epi unused: the consumer applies it)
+    GemvSeg seg[3];   // weights; seg.x_off = the segment's offset in the input planes
     int nseg;
-    int dual;            // seg0 = up, seg1 = gate: units interleaved per tile
-    InputSpec in;
-    int x_len;           // staged elements per batch row (>= every seg's x_off + kp)
-    const float* gamma;  // RMSNorm if non-null
+    int dual;         // seg0 = up, seg1 = gate: per tile, up lines then gate lines
+    Planes in;
+    const float* norm_src;  // non-null: output *= inv_rms(norm_src[b][0..norm_len)) (RMSNorm)
+    int norm_ld, norm_len;
     float eps;
-    int norm_len;
-    Pieces out;          // this phase's pieces
+    int out_kind;
+    Planes out;
+    int out_off[3];   // kOutPlanes: output offset of each segment's rows
+    float* xres;      // kOutResid: fp32 residual [B][xres_ld]
+    int xres_ld;
+    const float* gamma;  // kOutResid: the next RMSNorm's gamma
+    // kOutQKV
+    float* qbuf;      // [B][q_ld] RoPE'd q
+    int q_ld;
+    const float2* rope;  // [cap][d_head/2] (cos, sin), angles in double on the host
+    void* kcache;
+    void* vcache;
+    long long cache_bstride, cache_hstride;
+    int d_head;
+    const int* pos;
+    // kOutLogits
+    float* logits;    // [B][vocab]
+    int vocab;
+    float* cand_v;    // [tiles][B] best logit of each 16-row tile (ties -> lowest index)
+    int* cand_i;
+    // pieces exchange (per phase)
+    float* pieces;    // [out tile][max_pieces][subs][16][B]
+    unsigned* count;  // [out tile], zero between uses (self-resetting)
+    int max_pieces;
+    // chunk records in shared memory: [local tile < rec_ntl][sub][c < rec_c[sub]][16][B]
+    int rec_ntl, rec_c0, rec_c1;
 };
 
 struct MkAttn {
-    // q/k/v for the current position from the QKV-reconstruction pieces
-    Pieces pc;
-    int tbase_q, tbase_k, tbase_v;  // tiles of the q/k/v segments (each d_model rows)
-    const float2* rope;             // [cap][d_head/2]
-    const void* kcache;             // layer base [B][H][cap][d_head]
+    const float* qbuf;  // [B][q_ld] RoPE'd q of the current position
+    int q_ld;
+    const void* kcache;  // layer base [B][H][cap][d_head]
     const void* vcache;
     long long cache_bstride, cache_hstride;
-    const int* pos;
-    float* partial;                 // [B*H][splits][d_head + 4]: acc, l, m
+    const int* pos;      // attend rows 0 .. *pos
+    float* partial;      // [B*H][splits][d_head + 2]: acc, l, m
+    unsigned* count;     // [B*H]
     int n_heads, d_head, splits;
     float scale;
-    float* q_out;                   // optional debug copy of RoPE'd q [B][d] (nullptr: none)
+    Planes out;          // merged output (o-projection input)
 };
 
 struct MkArgmax {
-    Pieces pc;          // head pieces (one segment, tbase 0)
-    int vocab;
-    float* logits;      // [B][vocab]
-    float* best_v;      // [grid][B]
-    int* best_i;
-    unsigned* ticket;   // zeroed, self-resetting
-    int* tokens;        // [B] next input token
-    int* pos;           // length register
+    const float* cand_v;  // head tile candidates
+    const int* cand_i;
+    int ntiles;
+    int* tokens;          // [B] next input token
+    int* pos;             // length register
     int pos_inc;
-    int* out;           // generated tokens [B][out_ld] at column *step (may be null)
+    int* out;             // generated tokens [B][out_ld] at column *step (may be null)
     int out_ld;
     int* step;
 };
 
-struct MkPhase {
+struct MkVec {
+    const void* emb;     // embedding [V][emb_ld] (weight dtype), rows tokens[b]; or null
+    int emb_ld;
+    const int* tokens;
+    const float* src;    // else: fp32 [B][src_ld]
+    int src_ld;
+    int len;
+    float* xres;         // optional copy of the vector (the residual stream)
+    int xres_ld;
+    const float* gamma;  // planes = x * gamma
+    Planes out;
+};
+
+struct alignas(16) MkPhase {
     int kind;
     MkGemv g;
     MkAttn a;
     MkArgmax m;
+    MkVec v;
 };
 
 struct MkLaunch {
     const MkPhase* phases;  // device array
     int p_begin, p_end;
     unsigned* bar;          // zero-initialized grid-barrier counter (self-resetting)
-    int region_bytes;       // shared region carved per phase: x planes + unit partials
-    int red_floats;         // scratch: attention warp states / per-head merge records
     int grid, smem_bytes;
-    unsigned long long* trace;  // optional [grid][phases][8] globaltimer stamps (profiling)
+    int stages;             // ring depth (kChunkBytes each)
+    int x_bytes;            // staged input region
+    int rec_chunks;         // per-phase chunk records
+    unsigned long long* trace;  // optional [grid][phases][4] %globaltimer stamps
 };
 
-// Output tiles of a GEMV phase (dual: up tiles then gate tiles).
-int mk_out_tiles(const GemvSeg* seg, int nseg, int dual, int esize);
-// Host mirror of the device unit split: fills npieces[T] for every output
-// tile of a GEMV phase; returns the max (the phase's piece stride S).
-int mk_npieces(const GemvSeg* seg, int nseg, int dual, int esize, int grid, uint8_t* npieces);
-// Units of a GEMV phase (all segments).
+constexpr int kChunkLines = 8;                       // ring chunk: <= 8 lines of one tile
+constexpr int kChunkBytes = kChunkLines * kLineTileBytes;  // 16 KiB
+
+// ---- host mirrors of the device work split ----
+// Units (16-row x 128-byte lines) of a GEMV phase.
 int mk_units(const GemvSeg* seg, int nseg, int dual, int esize);
-int mk_region_bytes(int batch, WType wt, int x_len, int units_per_cta);
-int mk_red_floats(int batch, int n_heads, int d_head);
-int mk_smem_bytes(int region_bytes, int red_floats);
-int mk_warps();
+// Output tiles (dual: up/gate tile pairs count once).
+int mk_out_tiles(const GemvSeg* seg, int nseg, int dual, int esize);
+// Max CTAs contributing to one output tile; chunk-record shape of a CTA
+// (max local tiles, max chunks per run for sub 0 / 1).
+void mk_split_stats(const GemvSeg* seg, int nseg, int dual, int esize, int grid, int* max_pieces, int* rec_ntl,
+                    int* rec_c0, int* rec_c1);
+constexpr int kMkMaxLocalTiles = 64;
+int mk_smem_bytes(int stages, int x_bytes, int rec_chunks, int batch, int d_head);
+int mk_max_stages(int x_bytes, int rec_chunks, int batch, int d_head);
+int mk_consumer_warps();
 // false if (wt, batch, d_head) has no instantiation
 bool mk_launch(WType wt, int batch, int d_head, const MkLaunch& L, cudaStream_t s);
 

@@ -1,6 +1,5 @@
-// Shared pieces of the decode megakernel: PTX wrappers (mbarrier, bulk copy,
-// fences, mma), the shared-memory map, the unit split, and the phase-input
-// staging that resolves the producer's pieces + epilogue.
+// Shared pieces of the decode megakernel: PTX wrappers, the work split
+// (host + device), and the tensor-core chunk reduction.
 #pragma once
 
 #include <math_constants.h>
@@ -13,10 +12,9 @@ namespace fsvd::k::mk {
 
 using namespace fsvd::dev;
 
-constexpr int kWarpsMk = 8;
-constexpr int kThreadsMk = kWarpsMk * 32;
-constexpr int kSlots = 2;
-constexpr int kPrefetch = 6;  // L2-prefetch distance (units) beyond the shared-memory slots
+constexpr int kConsumerWarps = 8;
+constexpr int kConsumerThreads = kConsumerWarps * 32;
+constexpr int kThreads = kConsumerThreads + 32;  // + the producer warp
 
 // ------------------------------------------------------------ PTX helpers --
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
@@ -27,6 +25,9 @@ __device__ __forceinline__ void mbar_init(uint64_t* b, uint32_t count) {
 }
 __device__ __forceinline__ void mbar_expect_tx(uint64_t* b, uint32_t bytes) {
     asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(b)), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void mbar_arrive(uint64_t* b) {
+    asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(b)) : "memory");
 }
 __device__ __forceinline__ void mbar_wait(uint64_t* b, uint32_t parity) {
     asm volatile(
@@ -46,13 +47,20 @@ __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t by
         "l"(src), "r"(bytes), "r"(smem_u32(bar)), "l"(policy)
         : "memory");
 }
+__device__ __forceinline__ void bulk_g2s_plain(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
+    asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                     smem_u32(dst)),
+                 "l"(src), "r"(bytes), "r"(smem_u32(bar))
+                 : "memory");
+}
 __device__ __forceinline__ uint64_t evict_first_policy() {
     uint64_t p;
     asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(p));
     return p;
 }
-__device__ __forceinline__ void fence_proxy_async() { asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); }
-__device__ __forceinline__ void fence_acq_rel_gpu() { asm volatile("fence.acq_rel.gpu;" ::: "memory"); }
+__device__ __forceinline__ void fence_proxy_async_global() {
+    asm volatile("fence.proxy.async.global;" ::: "memory");
+}
 __device__ __forceinline__ unsigned long long gtimer() {
     unsigned long long t;
     asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
@@ -62,6 +70,18 @@ __device__ __forceinline__ unsigned ld_acquire(const unsigned* p) {
     unsigned v;
     asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
     return v;
+}
+__device__ __forceinline__ void fence_acq_rel_gpu() { asm volatile("fence.acq_rel.gpu;" ::: "memory"); }
+__device__ __forceinline__ unsigned atom_add_acq_rel(unsigned* p, unsigned v) {
+    unsigned old;
+    asm volatile("atom.acq_rel.gpu.global.add.u32 %0, [%1], %2;" : "=r"(old) : "l"(p), "r"(v) : "memory");
+    return old;
+}
+__device__ __forceinline__ void red_release_add(unsigned* p, unsigned v) {
+    asm volatile("red.release.gpu.global.add.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+__device__ __forceinline__ void consumer_sync() {
+    asm volatile("bar.sync 1, %0;" ::"n"(kConsumerThreads) : "memory");
 }
 // D(16x8, f32) += A(16x16, bf16, row) * B(16x8, bf16, col)
 __device__ __forceinline__ void mma_bf16(float* d, uint32_t a0, uint32_t a1, uint32_t a2, uint32_t a3, uint32_t b0,
@@ -75,275 +95,329 @@ __device__ __forceinline__ void mma_bf16(float* d, uint32_t a0, uint32_t a1, uin
 
 __device__ __forceinline__ bool better(float v, int i, float bv, int bi) { return v > bv || (v == bv && i < bi); }
 
-// ------------------------------------------------------------ unit split --
-__device__ __forceinline__ int unit_lo(int total, int c, int G) {
-    return static_cast<int>(static_cast<long long>(total) * c / G);
-}
-// CTA owning unit U
-__device__ __forceinline__ int unit_cta(int U, int total, int G) {
-    int c = static_cast<int>(static_cast<long long>(U) * G / total);
-    while (c + 1 < G && unit_lo(total, c + 1, G) <= U) ++c;
-    while (c > 0 && unit_lo(total, c, G) > U) --c;
-    return c;
-}
+}  // namespace fsvd::k::mk
 
-// --------------------------------------------------------- shared memory --
-struct Smem {
-    char* slots;     // [warp][kSlots][kUnitBytes]
-    uint64_t* full;  // [warp][kSlots]
-    void* x;         // per phase: bf16 [2B][x_len] hi/lo planes, or f32 [B][x_len]
-    int x_cap;       // elements per plane (this phase's x_len)
-    float* part;     // [CTA-local unit][16][B] partials
-    float* red;      // [kWarpsMk][d_head + 2] scratch
-    float* misc;     // 256 floats
-};
+namespace fsvd::k {
 
-template <typename W>
-struct XPlanes;
-// bf16 weights: x is staged as two bf16 planes per batch row, x = hi + lo
-// (RNE), the B operand of the tensor-core GEMV (column 2b = hi, 2b+1 = lo).
-template <>
-struct XPlanes<__nv_bfloat16> {
-    static constexpr int kPlanes = 2;
-    static __device__ __forceinline__ void put(const Smem& sm, int b, int i, float v) {
-        __nv_bfloat16* p = static_cast<__nv_bfloat16*>(sm.x);
-        const __nv_bfloat16 h = __float2bfloat16_rn(v);
-        p[(2 * b) * sm.x_cap + i] = h;
-        p[(2 * b + 1) * sm.x_cap + i] = __float2bfloat16_rn(v - __bfloat162float(h));
-    }
-};
-template <>
-struct XPlanes<float> {
-    static constexpr int kPlanes = 1;
-    static __device__ __forceinline__ void put(const Smem& sm, int b, int i, float v) {
-        static_cast<float*>(sm.x)[b * sm.x_cap + i] = v;
-    }
-};
+// ------------------------------------------------------------ work split --
+// Units of a GEMV phase are (16-row tile, 128-byte line) pairs numbered
+// segment by segment, tile-major, line-fastest; a dual phase interleaves per
+// tile: the up tile's lines, then the gate tile's. A "run" is the unit span
+// of one (output tile, sub) -- sub 1 = the gate half of a dual tile. CTA c
+// of G owns units [total*c/G, total*(c+1)/G); its chunks are <= kChunkLines
+// units of one run, starting at the run start or at the CTA's first unit.
+// All arithmetic is 32-bit (total * G < 2^32); the per-chunk walk is
+// incremental (ChunkIter) -- no divisions on the streaming path.
+struct MkSplit {
+    int total;
+    int nseg, dual;
+    int ubase[3];
+    int ntiles[3], nlines[3], tbase[3];
+    int out_tiles;
 
-// ---------------------------------------------------------------- pieces --
-__device__ __forceinline__ float4 ldcg4(const float* p) { return __ldcg(reinterpret_cast<const float4*>(p)); }
-__device__ __forceinline__ float4 add4(float4 a, float4 b) { return make_float4(a.x + b.x, a.y + b.y, a.z + b.z, a.w + b.w); }
-__device__ __forceinline__ float comp(const float4& v, int i) { return i == 0 ? v.x : (i == 1 ? v.y : (i == 2 ? v.z : v.w)); }
-
-// Sum of the S slot planes of pieces row r, batch b. The first four planes
-// are loaded together; the summation order is fixed (((p0+p1)+p2)+p3)+...
-template <int B>
-__device__ __forceinline__ float piece_sum(const Pieces& pc, int r, int b) {
-    const float* p = pc.base + static_cast<size_t>(r) * B + b;
-    const size_t pl = static_cast<size_t>(pc.R) * B;
-    const float p0 = __ldcg(p), p1 = pc.S > 1 ? __ldcg(p + pl) : 0.f;
-    const float p2 = pc.S > 2 ? __ldcg(p + 2 * pl) : 0.f, p3 = pc.S > 3 ? __ldcg(p + 3 * pl) : 0.f;
-    float s = ((p0 + p1) + p2) + p3;
-    for (int j = 4; j < pc.S; ++j) s += __ldcg(p + j * pl);
-    return s;
-}
-// The same for the 4 consecutive floats at row r (4/B rows x B), r aligned.
-template <int B>
-__device__ __forceinline__ float4 piece_sum4(const Pieces& pc, int r) {
-    const float* p = pc.base + static_cast<size_t>(r) * B;
-    const size_t pl = static_cast<size_t>(pc.R) * B;
-    const float4 z = make_float4(0.f, 0.f, 0.f, 0.f);
-    const float4 p0 = ldcg4(p), p1 = pc.S > 1 ? ldcg4(p + pl) : z;
-    const float4 p2 = pc.S > 2 ? ldcg4(p + 2 * pl) : z, p3 = pc.S > 3 ? ldcg4(p + 3 * pl) : z;
-    float4 s = add4(add4(add4(p0, p1), p2), p3);
-    for (int j = 4; j < pc.S; ++j) s = add4(s, ldcg4(p + j * pl));
-    return s;
-}
-
-// -------------------------------------------------------- input staging --
-// A "quad" = 4 consecutive floats of the [row][b] order: rows j0 .. j0+4/B-1
-// of input x for every batch row b. Quads never straddle a segment boundary
-// (segment offsets are multiples of 8); rows past a segment's logical rows
-// inside its last tile read pieces of zero-padded weight rows, i.e. 0.
-template <int B>
-__device__ __forceinline__ float4 src_quad(const float* src, int ld, int j0) {
-    if constexpr (B == 1) {
-        return __ldcg(reinterpret_cast<const float4*>(src + j0));
-    } else {
-        const float2 a = __ldcg(reinterpret_cast<const float2*>(src + j0));
-        const float2 b = __ldcg(reinterpret_cast<const float2*>(src + ld + j0));
-        return make_float4(a.x, b.x, a.y, b.y);
-    }
-}
-template <int B>
-__device__ __forceinline__ void dst_quad(float* dst, int ld, int j0, float4 v) {
-    if constexpr (B == 1) {
-        *reinterpret_cast<float4*>(dst + j0) = v;
-    } else {
-        *reinterpret_cast<float2*>(dst + j0) = make_float2(v.x, v.z);
-        *reinterpret_cast<float2*>(dst + ld + j0) = make_float2(v.y, v.w);
-    }
-}
-template <typename W, int B>
-__device__ __forceinline__ float4 emb_quad(const InputSpec& in, int j0) {
-    float o[4];
-#pragma unroll
-    for (int b = 0; b < B; ++b) {
-        const W* row = static_cast<const W*>(in.emb) + static_cast<long long>(__ldcg(in.tokens + b)) * in.emb_ld + j0;
-#pragma unroll
-        for (int rr = 0; rr < 4 / B; ++rr) o[rr * B + b] = to_f32<W>(row[rr]);
-    }
-    return make_float4(o[0], o[1], o[2], o[3]);
-}
-
-template <typename W, int B, int KIND>
-__device__ __forceinline__ float4 quad_value(const InputSpec& in, int j0) {
-    const float4 z = make_float4(0.f, 0.f, 0.f, 0.f);
-    if constexpr (KIND == kInPlain) {
-        return j0 < in.len ? src_quad<B>(in.src + 0, in.src_ld, j0) : z;
-    } else if constexpr (KIND == kInResidual) {
-        if (j0 >= in.len) return z;
-        const float4 x = src_quad<B>(in.src, in.src_ld, j0);
-        return in.nseg ? add4(x, piece_sum4<B>(in.seg[0].pc, (in.seg[0].tbase * 16 + j0) * 1)) : x;
-    } else if constexpr (KIND == kInEmbed) {
-        return j0 < in.len ? emb_quad<W, B>(in, j0) : z;
-    } else if constexpr (KIND == kInSilu) {
-        const int r = j0 - in.seg[0].x_off;
-        if (r < 0 || r >= in.seg[0].rows) return z;
-        const float4 u = piece_sum4<B>(in.seg[0].pc, in.seg[0].tbase * 16 + r);
-        const float4 g = piece_sum4<B>(in.seg[1].pc, in.seg[1].tbase * 16 + r);
-        return make_float4(silu_mul(g.x, u.x), silu_mul(g.y, u.y), silu_mul(g.z, u.z), silu_mul(g.w, u.w));
-    } else {  // kInPieces
-#pragma unroll
+    FSVD_HD void init(const GemvSeg* seg, int nseg_, int dual_, int es) {
+        nseg = nseg_;
+        dual = dual_;
+        int u = 0, t = 0;
         for (int s = 0; s < 3; ++s) {
-            if (s >= in.nseg) break;
-            const int r = j0 - in.seg[s].x_off;
-            if (r >= 0 && r < in.seg[s].rows) return piece_sum4<B>(in.seg[s].pc, in.seg[s].tbase * 16 + r);
+            ntiles[s] = nlines[s] = tbase[s] = 0;
+            ubase[s] = u;
+            if (s >= nseg) continue;
+            const WLayout l = seg[s].layout(es);
+            ntiles[s] = l.ntiles();
+            nlines[s] = l.nlines();
+            tbase[s] = t;
+            if (!dual) {
+                u += ntiles[s] * nlines[s];
+                t += ntiles[s];
+            }
         }
-        return z;
+        if (dual) {
+            total = ntiles[0] * (nlines[0] + nlines[1]);
+            out_tiles = ntiles[0];
+        } else {
+            total = u;
+            out_tiles = t;
+        }
     }
-}
-
-// Stage quads of x into the shared planes (times gamma when the phase
-// RMSNorms); residual kinds write their CTA's share of quads back to dst.
-template <typename W, int B, int KIND>
-__device__ void stage_loop(const MkGemv& g, const Smem& sm, int tid, int cta, int ncta, float* ss) {
-    constexpr int RQ = 4 / B, QB = 4;
-    const InputSpec& in = g.in;
-    const int nq = g.x_len / RQ;
-    const int nql = in.len / RQ;  // quads of the written-back residual
-    const int w0 = unit_lo(nql, cta, ncta), w1 = unit_lo(nql, cta + 1, ncta);
-    for (int q0 = tid; q0 < nq; q0 += QB * kThreadsMk) {
-        float4 v[QB];
-#pragma unroll
-        for (int u = 0; u < QB; ++u) {
-            const int q = q0 + u * kThreadsMk;
-            v[u] = q < nq ? quad_value<W, B, KIND>(in, q * RQ) : make_float4(0.f, 0.f, 0.f, 0.f);
+    FSVD_HD int subs() const { return dual ? 2 : 1; }
+    FSVD_HD int lo(int c, int G) const {
+        return static_cast<int>(static_cast<unsigned>(total) * static_cast<unsigned>(c) / static_cast<unsigned>(G));
+    }
+    FSVD_HD int seg_of_tile(int T) const {
+        int s = 0;
+        if (!dual)
+            while (s + 1 < nseg && T >= tbase[s + 1]) ++s;
+        return s;
+    }
+    // unit span of output tile T (both subs for dual)
+    FSVD_HD void tile_span(int T, int& a, int& e) const {
+        if (dual) {
+            const int per = nlines[0] + nlines[1];
+            a = T * per;
+            e = a + per;
+            return;
         }
+        const int s = seg_of_tile(T);
+        a = ubase[s] + (T - tbase[s]) * nlines[s];
+        e = a + nlines[s];
+    }
+    // unit span of run (T, sub)
+    FSVD_HD void run_span(int T, int sub, int& a, int& e) const {
+        tile_span(T, a, e);
+        if (dual) {
+            if (sub == 0)
+                e = a + nlines[0];
+            else
+                a += nlines[0];
+        }
+    }
+    // output tile of unit U
+    FSVD_HD int tile_of(int U) const {
+        if (dual) return U / (nlines[0] + nlines[1]);
+        int s = 0;
+        while (s + 1 < nseg && U >= ubase[s + 1]) ++s;
+        return tbase[s] + (U - ubase[s]) / nlines[s];
+    }
+    // CTA owning unit U (non-empty range)
+    FSVD_HD int cta_of(int U, int G) const {
+        int c = static_cast<int>(static_cast<unsigned>(U) * static_cast<unsigned>(G) / static_cast<unsigned>(total));
+        if (c >= G) c = G - 1;
+        while (c + 1 < G && lo(c + 1, G) <= U) ++c;
+        while (c > 0 && lo(c, G) > U) --c;
+        return c;
+    }
+    // number of non-empty CTAs in [c0, c1)
+    FSVD_HD int nonempty(int c0, int c1, int G) const {
+        int n = 0;
+        int l = lo(c0, G);
+        for (int c = c0; c < c1; ++c) {
+            const int h = lo(c + 1, G);
+            n += h > l;
+            l = h;
+        }
+        return n;
+    }
+    // chunks of run span [a, e) inside [ulo, uhi)
+    static FSVD_HD int run_chunks(int a, int e, int ulo, int uhi) {
+        const int x = a > ulo ? a : ulo, y = e < uhi ? e : uhi;
+        return y > x ? (y - x + kChunkLines - 1) / kChunkLines : 0;
+    }
+};
+
+// Incremental walk over one CTA's chunks of a phase (shared by the producer
+// and the consumers, so both see the same chunk sequence).
+struct ChunkIter {
+    int U, uhi;
+    int s, t, line;  // segment (dual: sub), tile within segment, line within run
+    FSVD_HD void begin(const MkSplit& sp, int ulo, int uhi_) {
+        U = ulo;
+        uhi = uhi_;
+        if (U >= uhi) return;
+        if (sp.dual) {
+            const int per = sp.nlines[0] + sp.nlines[1];
+            t = U / per;
+            const int rem = U - t * per;
+            s = rem < sp.nlines[0] ? 0 : 1;
+            line = s ? rem - sp.nlines[0] : rem;
+        } else {
+            s = 0;
+            while (s + 1 < sp.nseg && U >= sp.ubase[s + 1]) ++s;
+            const int rel = U - sp.ubase[s];
+            t = rel / sp.nlines[s];
+            line = rel - t * sp.nlines[s];
+        }
+    }
+    FSVD_HD bool done() const { return U >= uhi; }
+    // lines of the current chunk
+    FSVD_HD int lines(const MkSplit& sp) const {
+        int n = sp.nlines[s] - line;
+        if (n > kChunkLines) n = kChunkLines;
+        if (n > uhi - U) n = uhi - U;
+        return n;
+    }
+    FSVD_HD void advance(const MkSplit& sp, int nl) {
+        U += nl;
+        line += nl;
+        if (line < sp.nlines[s]) return;
+        line = 0;
+        if (sp.dual) {
+            if (s == 0) {
+                s = 1;
+            } else {
+                s = 0;
+                ++t;
+            }
+        } else if (++t == sp.ntiles[s]) {
+            t = 0;
+            ++s;
+        }
+    }
+};
+
+// A CTA's chunk sequence in "boundary tiles first" order: the first tile of
+// its range, then the last, then the interior -- so the per-CTA partials of
+// the two tiles shared with neighbouring CTAs are exchanged while the
+// interior still streams. Every tile's chunks stay contiguous.
+struct ChunkSeq {
+    int r_lo[3], r_hi[3];
+    int nr, r;
+    ChunkIter it;
+    int c_run;  // chunk index inside the current run
+    FSVD_HD void begin(const MkSplit& sp, int ulo, int uhi) {
+        nr = 0;
+        if (ulo < uhi) {
+            const int Tf = sp.tile_of(ulo), Tl = sp.tile_of(uhi - 1);
+            int a, e, a2, e2;
+            sp.tile_span(Tf, a, e);
+            sp.tile_span(Tl, a2, e2);
+            const int ef = e < uhi ? e : uhi;
+            r_lo[nr] = ulo; r_hi[nr] = ef; ++nr;
+            if (Tl > Tf) {
+                r_lo[nr] = a2; r_hi[nr] = uhi; ++nr;
+                if (a2 > ef) { r_lo[nr] = ef; r_hi[nr] = a2; ++nr; }
+            }
+        }
+        r = 0;
+        c_run = 0;
+        if (nr) it.begin(sp, r_lo[0], r_hi[0]);
+        else it.U = it.uhi = 0;
+    }
+    FSVD_HD bool done() const { return r >= nr; }
+    FSVD_HD int tile(const MkSplit& sp) const { return sp.dual ? it.t : sp.tbase[it.s] + it.t; }
+    FSVD_HD int sub(const MkSplit& sp) const { return sp.dual ? it.s : 0; }
+    // advance past the current chunk of nl lines
+    FSVD_HD void advance(const MkSplit& sp, int nl) {
+        const int line0 = it.line;
+        it.advance(sp, nl);
+        (void)line0;
+        c_run = it.line == 0 ? 0 : c_run + 1;
+        if (it.done()) {
+            ++r;
+            c_run = 0;
+            if (r < nr) it.begin(sp, r_lo[r], r_hi[r]);
+        }
+    }
+};
+
+// Same split over a plain row space (attention: B*H*len key rows).
+struct RowSplit {
+    int total;
+    FSVD_HD int lo(int c, int G) const {
+        return static_cast<int>(static_cast<unsigned>(total) * static_cast<unsigned>(c) / static_cast<unsigned>(G));
+    }
+    FSVD_HD int cta_of(int U, int G) const {
+        int c = static_cast<int>(static_cast<unsigned>(U) * static_cast<unsigned>(G) / static_cast<unsigned>(total));
+        if (c >= G) c = G - 1;
+        while (c + 1 < G && lo(c + 1, G) <= U) ++c;
+        while (c > 0 && lo(c, G) > U) --c;
+        return c;
+    }
+    FSVD_HD int nonempty(int c0, int c1, int G) const {
+        int n = 0;
+        int l = lo(c0, G);
+        for (int c = c0; c < c1; ++c) {
+            const int h = lo(c + 1, G);
+            n += h > l;
+            l = h;
+        }
+        return n;
+    }
+};
+
+}  // namespace fsvd::k
+
+namespace fsvd::k::mk {
+
+// ---------------------------------------------------------- chunk compute --
+// 16 row partials of one chunk (nl lines of a tile) for each batch row ->
+// rec[(row)*B + b]. bf16: tensor cores, mma.sync m16n8k16 with the 16
+// weight rows as A and the staged x planes as B (column 2b = hi, 2b+1 = lo);
+// k is permuted inside each 16-wide step so that every A and B fragment is
+// one 8-byte, bank-conflict-free shared load (the XOR swizzle of layout.h).
+template <typename W, int B>
+struct ChunkDot;
+
+template <int B>
+struct ChunkDot<__nv_bfloat16, B> {
+    static __device__ __forceinline__ void run(const char* buf, int nl, const __nv_bfloat16* x, int x_len, int kbase,
+                                               int lane, float* rec) {
+        const int g = lane >> 2, t = lane & 3;
+        const __nv_bfloat16* xp = x + g * x_len + kbase + 4 * t;
+        float d[4][4] = {};
+#pragma unroll 2
+        for (int l = 0; l < nl; ++l) {
+            const char* lb = buf + l * kLineTileBytes;
 #pragma unroll
-        for (int u = 0; u < QB; ++u) {
-            const int q = q0 + u * kThreadsMk;
-            if (q >= nq) break;
-            const int j0 = q * RQ;
-            if constexpr (KIND == kInResidual || KIND == kInEmbed)
-                if (in.dst && q >= w0 && q < w1) dst_quad<B>(in.dst, in.dst_ld, j0, v[u]);
+            for (int j = 0; j < 4; ++j) {
+                const int off = ((((2 * j + (t >> 1)) ^ g) & 7) << 4) | ((t & 1) << 3);
+                const uint2 r0 = *reinterpret_cast<const uint2*>(lb + g * kLineBytes + off);
+                const uint2 r1 = *reinterpret_cast<const uint2*>(lb + (g + 8) * kLineBytes + off);
+                uint2 xv = make_uint2(0u, 0u);
+                if (g < 2 * B) xv = *reinterpret_cast<const uint2*>(xp + l * 64 + 16 * j);
+                mma_bf16(d[j], r0.x, r1.x, r0.y, r1.y, xv.x, xv.y);
+            }
+        }
+        if (t < B) {
+            rec[g * B + t] = ((d[0][0] + d[1][0]) + (d[2][0] + d[3][0])) + ((d[0][1] + d[1][1]) + (d[2][1] + d[3][1]));
+            rec[(g + 8) * B + t] =
+                ((d[0][2] + d[1][2]) + (d[2][2] + d[3][2])) + ((d[0][3] + d[1][3]) + (d[2][3] + d[3][3]));
+        }
+    }
+};
+
+// fp32 weights (parity mode): exact CUDA-core dot, 2 lanes per row
+template <int B>
+struct ChunkDot<float, B> {
+    static __device__ __forceinline__ void run(const char* buf, int nl, const float* x, int x_len, int kbase, int lane,
+                                               float* rec) {
+        const int i = lane >> 1, h = lane & 1;
+        float acc[B];
 #pragma unroll
-            for (int rr = 0; rr < RQ; ++rr) {
-                const int j = j0 + rr;
-                const float gm = g.gamma ? (j < g.norm_len ? g.gamma[j] : 0.f) : 1.f;
+        for (int b = 0; b < B; ++b) acc[b] = 0.f;
+        for (int l = 0; l < nl; ++l) {
+#pragma unroll
+            for (int cc = 0; cc < 4; ++cc) {
+                const int c = h * 4 + cc;
+                const float4 w = *reinterpret_cast<const float4*>(buf + l * kLineTileBytes + i * kLineBytes +
+                                                                  (((c ^ (i & 7)) & 7) << 4));
 #pragma unroll
                 for (int b = 0; b < B; ++b) {
-                    const float x = comp(v[u], rr * B + b);
-                    ss[b] = fmaf(x, x, ss[b]);
-                    XPlanes<W>::put(sm, b, j, x * gm);
+                    const float4 xv = *reinterpret_cast<const float4*>(x + b * x_len + kbase + l * 32 + c * 4);
+                    acc[b] = fmaf(w.x, xv.x, acc[b]);
+                    acc[b] = fmaf(w.y, xv.y, acc[b]);
+                    acc[b] = fmaf(w.z, xv.z, acc[b]);
+                    acc[b] = fmaf(w.w, xv.w, acc[b]);
                 }
             }
         }
+#pragma unroll
+        for (int b = 0; b < B; ++b) {
+            acc[b] += __shfl_xor_sync(0xffffffffu, acc[b], 1);
+            if (h == 0) rec[i * B + b] = acc[b];
+        }
     }
-}
+};
 
-// Attention merge: x[b][h*dh + e] = sum_c acc_c[e] exp(m_c - M) / sum_c l_c exp(m_c - M)
-// over the CTAs c whose cache-row range intersected head (b, h), in CTA
-// order (slot j = j-th such CTA). sm.red: per head (M, 1/L, n).
-template <typename W, int B>
-__device__ void stage_attn(const InputSpec& in, const Smem& sm, int tid, int ncta) {
-    const AttnMerge& am = in.am;
-    const int dh = am.d_head, H = am.n_heads, st = dh + 4;
-    const int len = *am.pos + 1;
-    const long long N = static_cast<long long>(B) * H * len;
-    float* rec = sm.red;
-    for (int bh = tid; bh < B * H; bh += kThreadsMk) {
-        const long long lo_bh = static_cast<long long>(bh) * len, hi_bh = lo_bh + len;
-        int c = static_cast<int>(lo_bh * ncta / N);
-        while (c > 0 && N * c / ncta > lo_bh) --c;
-        int n = 0;
-        for (; c < ncta; ++c) {
-            const long long s0 = N * c / ncta, s1 = N * (c + 1) / ncta;
-            if (s0 >= hi_bh) break;
-            if ((s0 > lo_bh ? s0 : lo_bh) < (s1 < hi_bh ? s1 : hi_bh)) ++n;
-        }
-        const float* pb = am.partial + static_cast<long long>(bh) * am.splits * st;
-        float M = -CUDART_INF_F;
-        for (int j = 0; j < n; ++j) M = fmaxf(M, __ldcg(pb + j * st + dh + 1));
-        float L = 0.f;
-        for (int j = 0; j < n; ++j) L += __ldcg(pb + j * st + dh) * expf(__ldcg(pb + j * st + dh + 1) - M);
-        rec[bh * 3 + 0] = M;
-        rec[bh * 3 + 1] = 1.0f / L;
-        rec[bh * 3 + 2] = __int_as_float(n);
+// ------------------------------------------------------- planes writers --
+template <typename W>
+struct PlaneIO;
+template <>
+struct PlaneIO<__nv_bfloat16> {
+    static constexpr int kBytesPerElem = 4;  // hi + lo
+    static __device__ __forceinline__ void put(const Planes& p, int b, int i, float v) {
+        __nv_bfloat16* q = static_cast<__nv_bfloat16*>(p.p) + static_cast<size_t>(2 * b) * p.len;
+        const __nv_bfloat16 h = __float2bfloat16_rn(v);
+        q[i] = h;
+        q[p.len + i] = __float2bfloat16_rn(v - __bfloat162float(h));
     }
-    __syncthreads();
-    const int qph = dh / 4;
-    for (int qq = tid; qq < B * H * qph; qq += kThreadsMk) {
-        const int bh = qq / qph, e = (qq - bh * qph) * 4;
-        const float M = rec[bh * 3], inv = rec[bh * 3 + 1];
-        const int n = __float_as_int(rec[bh * 3 + 2]);
-        const float* pb = am.partial + static_cast<long long>(bh) * am.splits * st;
-        float4 o = make_float4(0.f, 0.f, 0.f, 0.f);
-        for (int j = 0; j < n; ++j) {
-            const float w = expf(__ldcg(pb + j * st + dh + 1) - M);
-            const float4 a = ldcg4(pb + j * st + e);
-            o.x = fmaf(a.x, w, o.x);
-            o.y = fmaf(a.y, w, o.y);
-            o.z = fmaf(a.z, w, o.z);
-            o.w = fmaf(a.w, w, o.w);
-        }
-        const int b = bh / H, hh = bh - b * H;
-        XPlanes<W>::put(sm, b, hh * dh + e + 0, o.x * inv);
-        XPlanes<W>::put(sm, b, hh * dh + e + 1, o.y * inv);
-        XPlanes<W>::put(sm, b, hh * dh + e + 2, o.z * inv);
-        XPlanes<W>::put(sm, b, hh * dh + e + 3, o.w * inv);
+};
+template <>
+struct PlaneIO<float> {
+    static constexpr int kBytesPerElem = 4;
+    static __device__ __forceinline__ void put(const Planes& p, int b, int i, float v) {
+        static_cast<float*>(p.p)[static_cast<size_t>(b) * p.len + i] = v;
     }
-}
-
-// Stage this phase's input x (producer epilogue applied; times gamma when the
-// phase RMSNorms) and compute inv_rms into misc[128 + b].
-template <typename W, int B>
-__device__ void stage_x(const MkGemv& g, const Smem& sm, int tid, int cta, int ncta) {
-    const InputSpec& in = g.in;
-    float ss[B];
-#pragma unroll
-    for (int b = 0; b < B; ++b) ss[b] = 0.f;
-    switch (in.kind) {
-        case kInAttn: {
-            stage_attn<W, B>(in, sm, tid, ncta);
-            const int H_dh = in.am.n_heads * in.am.d_head;
-            for (int j = H_dh + tid; j < g.x_len; j += kThreadsMk)
-#pragma unroll
-                for (int b = 0; b < B; ++b) XPlanes<W>::put(sm, b, j, 0.f);
-            break;
-        }
-        case kInPlain: stage_loop<W, B, kInPlain>(g, sm, tid, cta, ncta, ss); break;
-        case kInResidual: stage_loop<W, B, kInResidual>(g, sm, tid, cta, ncta, ss); break;
-        case kInEmbed: stage_loop<W, B, kInEmbed>(g, sm, tid, cta, ncta, ss); break;
-        case kInSilu: stage_loop<W, B, kInSilu>(g, sm, tid, cta, ncta, ss); break;
-        default: stage_loop<W, B, kInPieces>(g, sm, tid, cta, ncta, ss); break;
-    }
-    if (g.gamma) {
-#pragma unroll
-        for (int b = 0; b < B; ++b) ss[b] = warp_sum(ss[b]);
-        if ((tid & 31) == 0)
-#pragma unroll
-            for (int b = 0; b < B; ++b) sm.misc[(tid >> 5) * 4 + b] = ss[b];
-        __syncthreads();
-        if (tid < B) {
-            float t = 0.f;
-            for (int w = 0; w < kWarpsMk; ++w) t += sm.misc[w * 4 + tid];
-            sm.misc[128 + tid] = 1.0f / sqrtf(t / static_cast<float>(g.norm_len) + g.eps);
-        }
-    } else if (tid < B) {
-        sm.misc[128 + tid] = 1.f;
-    }
-    __syncthreads();
-}
+};
 
 }  // namespace fsvd::k::mk

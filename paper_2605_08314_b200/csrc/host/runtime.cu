@@ -441,14 +441,16 @@ Session::Session(DeviceModel* m, const fsvd_session_opts& o) : m_(m) {
     }
     ld_qkv_ = pad8(ld_qkv_);
     ld_ug_ = pad8(ld_ug_);
-    xres_[0] = static_cast<float*>(dalloc(4ull * B_ * m->ldd));
-    xres_[1] = static_cast<float*>(dalloc(4ull * B_ * m->ldd));
+    xres_ = static_cast<float*>(dalloc(4ull * B_ * m->ldd));
     x_ = static_cast<float*>(dalloc(4ull * B_ * m->ldd));
     logits_ = static_cast<float*>(dalloc(4ull * B_ * c.vocab));
 
     mk_grid_ = m->sm_count;
+    if (const char* g = std::getenv("FSVD_MK_GRID"); g && std::atoi(g) > 0)  // debugging: fewer CTAs
+        mk_grid_ = std::min(mk_grid_, std::atoi(g));
     mk_splits_ = mk_grid_;  // attention partial slots per head: one per contributing CTA
-    attn_part_ = static_cast<float*>(dalloc(4ull * B_ * H * mk_splits_ * (dh + 4)));
+    attn_part_ = static_cast<float*>(dalloc(4ull * B_ * H * mk_splits_ * (dh + 2)));
+    attn_count_ = static_cast<unsigned*>(dalloc(4ull * B_ * H));
     build_program();
     FSVD_CUDA(cudaStreamSynchronize(stream_));
     stats_.allocs = 0;
@@ -478,11 +480,18 @@ void* Session::staging(size_t bytes) {
 }
 
 // ------------------------------------------------------------ phase program --
-// Appends one GEMV phase; returns where its pieces live. in_refs[s] is the
-// producer of in.seg[s] (the device pointers are patched in after every
-// phase is known and the buffers are sized).
-Session::PieceRef Session::add_gemv(const std::vector<k::GemvSeg>& segs, int dual, k::InputSpec in,
-                                    const std::vector<PieceRef>& in_refs, int x_len, const float* gamma) {
+// Activation vector in the megakernel's B-operand form (decode_mk.h Planes):
+// 4 bytes per element and batch row (bf16 hi + lo, or fp32), zero padded.
+k::Planes Session::planes(int len) {
+    const int l = pad64(static_cast<size_t>(len));
+    x_bytes_ = std::max(x_bytes_, B_ * l * 4);
+    return k::Planes{dalloc(4ull * B_ * l), l};
+}
+
+// Appends one GEMV phase (weights segs, input planes in); the caller fills
+// the output side. Allocates the phase's pieces exchange.
+k::MkGemv& Session::add_gemv(const std::vector<k::GemvSeg>& segs, int dual, const k::Planes& in,
+                             const float* norm_src, int out_kind) {
     const DeviceModel& m = *m_;
     k::MkPhase p{};
     p.kind = k::kMkGemv;
@@ -491,247 +500,203 @@ Session::PieceRef Session::add_gemv(const std::vector<k::GemvSeg>& segs, int dua
     g.nseg = static_cast<int>(segs.size());
     g.dual = dual;
     g.in = in;
-    g.x_len = x_len;
-    g.gamma = gamma;
-    g.eps = static_cast<float>(m.cfg.norm_eps);
+    for (int i = 0; i < g.nseg; ++i)
+        if (g.seg[i].x_off + g.seg[i].kp > in.len) throw std::logic_error("megakernel: input planes too short");
+    g.norm_src = norm_src;
+    g.norm_ld = m.ldd;
     g.norm_len = static_cast<int>(m.cfg.d_model);
-    // every GEMV phase owns its pieces buffer (unused slots stay zero)
+    g.eps = static_cast<float>(m.cfg.norm_eps);
+    g.out_kind = out_kind;
+    int max_pieces = 1;
+    k::mk_split_stats(g.seg, g.nseg, dual, m.esize, mk_grid_, &max_pieces, &g.rec_ntl, &g.rec_c0, &g.rec_c1);
+    if (g.rec_ntl > k::kMkMaxLocalTiles)
+        throw ConfigError("decode megakernel: a CTA would touch more than 64 output tiles of one phase");
+    const int max_chunks = g.rec_ntl * (g.rec_c0 + g.rec_c1);
     const int nt = k::mk_out_tiles(g.seg, g.nseg, dual, m.esize);
-    std::vector<uint8_t> np(nt);
-    PieceRef r{0, 0, 0, nt * k::kTileRows};
-    r.S = k::mk_npieces(g.seg, g.nseg, dual, m.esize, mk_grid_, np.data());
-    r.off = piece_floats_;
-    piece_floats_ += (static_cast<size_t>(r.R) * r.S * B_ + 63) / 64 * 64;
-    const int units = k::mk_units(g.seg, g.nseg, dual, m.esize);
-    const int per_cta = (units + mk_grid_ - 1) / mk_grid_ + 1;
-    region_max_ = std::max(region_max_, k::mk_region_bytes(B_, m.wt, x_len, per_cta));
+    g.max_pieces = max_pieces;
+    g.pieces = static_cast<float*>(dalloc(4ull * nt * max_pieces * 2 * k::kTileRows * B_));
+    g.count = static_cast<unsigned*>(dalloc(4ull * nt));
+    rec_chunks_ = std::max(rec_chunks_, max_chunks);
     if (h_phases_.size() == h_phases_.capacity()) throw std::logic_error("phase program capacity");
     h_phases_.push_back(p);
-    k::MkGemv& G = h_phases_.back().g;
-    fix(&G.out, r);
-    for (size_t i = 0; i < in_refs.size(); ++i) fix(&G.in.seg[i].pc, in_refs[i]);
-    return r;
+    return h_phases_.back().g;
 }
 
-namespace {
-k::InSeg inseg(int x_off, int rows, int tbase) {
-    k::InSeg s{};
-    s.x_off = x_off;
-    s.rows = rows;
-    s.tbase = tbase;
-    return s;
+int Session::add_vec(const void* emb, const float* src, float* xres, const float* gamma, const k::Planes& out) {
+    const DeviceModel& m = *m_;
+    k::MkPhase p{};
+    p.kind = k::kMkVec;
+    k::MkVec& v = p.v;
+    v.emb = emb;
+    v.emb_ld = m.ldd;
+    v.tokens = tokens_;
+    v.src = src;
+    v.src_ld = m.ldd;
+    v.len = static_cast<int>(m.cfg.d_model);
+    v.xres = xres;
+    v.xres_ld = m.ldd;
+    v.gamma = gamma;
+    v.out = out;
+    h_phases_.push_back(p);
+    return static_cast<int>(h_phases_.size()) - 1;
 }
-int tiles(int rows) { return (rows + k::kTileRows - 1) / k::kTileRows; }
-}  // namespace
 
-// One layer: prev = the down projection's pieces of the
-// previous layer (buf < 0: layer 0 starts from the embedding).
-void Session::add_layer_phases(size_t l, PieceRef& prev) {
+// One layer. Input: xpl_ = rmsnorm gamma-scaled residual
+// planes (the scale 1/rms is applied to the projection outputs); output: the
+// residual xres_ and xpl_ scaled by the next norm's gamma (next_gamma).
+void Session::add_layer_phases(size_t l, const float* next_gamma) {
     const DeviceModel& m = *m_;
     const ModelConfig& c = m.cfg;
     const DeviceLayer& L = m.layers[l];
-    const int d = static_cast<int>(c.d_model), dff = static_cast<int>(c.d_ff);
     char* kc = static_cast<char*>(kc_) + l * cache_lstride_ * m.esize;
     char* vc = static_cast<char*>(vc_) + l * cache_lstride_ * m.esize;
     const int rq = L.rp[kQ], rk = L.rp[kK];
-    // residual stream: qkvA reads x = X[0] + prev (or the embedding), writes X[1]
-    k::InputSpec res{};
-    std::vector<PieceRef> res_refs;
-    if (prev.buf < 0) {
-        res.kind = k::kInEmbed;
-        res.emb = m.emb;
-        res.emb_ld = m.ldd;
-        res.tokens = tokens_;
-    } else {
-        res.kind = k::kInResidual;
-        res.src = xres_[0];
-        res.src_ld = m.ldd;
-        res.seg[0] = inseg(0, d, 0);
-        res.nseg = 1;
-        res_refs.push_back(prev);
-    }
-    res.len = d;
-    res.dst = xres_[1];
-    res.dst_ld = m.ldd;
     // qkvA: p_qkv = rmsnorm(x) . [A_q | A_k | A_v]   (packed QKV projection)
-    const PieceRef qkvA = add_gemv({seg(L.at[kQ], 0, 0, 0), seg(L.at[kK], 0, 0, 0), seg(L.at[kV], 0, 0, 0)}, 0, res,
-                                   res_refs, L.at[kQ].kp, L.attn_gamma);
-    // qkvB: q, k, v = p . B  (RoPE and the cache append happen in the attention prologue)
-    PieceRef qkvB;
     {
-        k::InputSpec in{};
-        in.kind = k::kInPieces;
-        in.seg[0] = inseg(0, L.r[kQ], 0);
-        in.seg[1] = inseg(rq, L.r[kK], tiles(L.r[kQ]));
-        in.seg[2] = inseg(rq + rk, L.r[kV], tiles(L.r[kQ]) + tiles(L.r[kK]));
-        in.nseg = 3;
-        qkvB = add_gemv({seg(L.bt[kQ], 0, 0, 0), seg(L.bt[kK], rq, 0, 0), seg(L.bt[kV], rq + rk, 0, 0)}, 0, in,
-                        {qkvA, qkvA, qkvA}, rq + rk + L.bt[kV].kp, nullptr);
+        k::MkGemv& g = add_gemv({seg(L.at[kQ], 0, 0, 0), seg(L.at[kK], 0, 0, 0), seg(L.at[kV], 0, 0, 0)}, 0, xpl_,
+                                xres_, k::kOutPlanes);
+        g.out = pqkv_;
+        g.out_off[0] = 0;
+        g.out_off[1] = rq;
+        g.out_off[2] = rq + rk;
+    }
+    // qkvB: q, k, v = p . B with RoPE (q, k) and the dense-KV append at pos
+    {
+        k::MkGemv& g = add_gemv({seg(L.bt[kQ], 0, 0, 0), seg(L.bt[kK], rq, 0, 0), seg(L.bt[kV], rq + rk, 0, 0)}, 0,
+                                pqkv_, nullptr, k::kOutQKV);
+        g.qbuf = qbuf_;
+        g.q_ld = m.ldd;
+        g.rope = rope_;
+        g.kcache = kc;
+        g.vcache = vc;
+        g.cache_bstride = cache_bstride_;
+        g.cache_hstride = cache_hstride_;
+        g.d_head = static_cast<int>(c.d_head);
+        g.pos = pos_;
     }
     // dense-KV attention over cache rows [0, pos]
     {
         k::MkPhase p{};
         p.kind = k::kMkAttn;
         k::MkAttn& a = p.a;
-        a.tbase_q = 0;
-        a.tbase_k = tiles(d);
-        a.tbase_v = 2 * tiles(d);
-        a.rope = rope_;
+        a.qbuf = qbuf_;
+        a.q_ld = m.ldd;
         a.kcache = kc;
         a.vcache = vc;
         a.cache_bstride = cache_bstride_;
         a.cache_hstride = cache_hstride_;
         a.pos = pos_;
         a.partial = attn_part_;
+        a.count = attn_count_;
         a.n_heads = static_cast<int>(c.n_heads);
         a.d_head = static_cast<int>(c.d_head);
         a.splits = mk_splits_;
         a.scale = static_cast<float>(1.0 / std::sqrt(static_cast<double>(c.d_head)));
+        a.out = att_;
         h_phases_.push_back(p);
-        fix(&h_phases_.back().a.pc, qkvB);
     }
-    // o projection; the residual add happens in the next phase's staging
-    PieceRef oA, oB;
+    // o projection, residual add (+ the FFN norm's gamma)
+    add_gemv({seg(L.at[kO], 0, 0, 0)}, 0, att_, nullptr, k::kOutPlanes).out = po_;
     {
-        k::InputSpec in{};
-        in.kind = k::kInAttn;
-        in.am = {attn_part_, static_cast<int>(c.n_heads), static_cast<int>(c.d_head), mk_splits_, pos_};
-        oA = add_gemv({seg(L.at[kO], 0, 0, 0)}, 0, in, {}, L.at[kO].kp, nullptr);
+        k::MkGemv& g = add_gemv({seg(L.bt[kO], 0, 0, 0)}, 0, po_, nullptr, k::kOutResid);
+        g.out = xpl_;
+        g.xres = xres_;
+        g.xres_ld = m.ldd;
+        g.gamma = L.mlp_gamma;
     }
-    {
-        k::InputSpec in{};
-        in.kind = k::kInPieces;
-        in.seg[0] = inseg(0, L.r[kO], 0);
-        in.nseg = 1;
-        oB = add_gemv({seg(L.bt[kO], 0, 0, 0)}, 0, in, {oA}, L.bt[kO].kp, nullptr);
-    }
-    // FFN input side: x = X[1] + o, written to X[0]; packed = one projection over [A_up | A_gate]
-    k::InputSpec r2{};
-    r2.kind = k::kInResidual;
-    r2.src = xres_[1];
-    r2.src_ld = m.ldd;
-    r2.len = d;
-    r2.dst = xres_[0];
-    r2.dst_ld = m.ldd;
-    r2.seg[0] = inseg(0, d, 0);
-    r2.nseg = 1;
-    k::InputSpec ugb{};
-    ugb.kind = k::kInPieces;
-    ugb.nseg = 2;
-    std::vector<PieceRef> ugb_refs;
+    // FFN input side: packed = one projection over [A_up | A_gate]
     if (ffn_ == FSVD_FFN_PACKED) {
-        const PieceRef ug =
-            add_gemv({seg(L.at[kUp], 0, 0, 0), seg(L.at[kGate], 0, 0, 0)}, 0, r2, {oB}, L.at[kUp].kp, L.mlp_gamma);
-        ugb.seg[0] = inseg(0, L.r[kUp], 0);
-        ugb.seg[1] = inseg(L.rp[kUp], L.r[kGate], tiles(L.r[kUp]));
-        ugb_refs = {ug, ug};
+        k::MkGemv& g = add_gemv({seg(L.at[kUp], 0, 0, 0), seg(L.at[kGate], 0, 0, 0)}, 0, xpl_, xres_, k::kOutPlanes);
+        g.out = pug_;
+        g.out_off[1] = L.rp[kUp];
     } else {
-        const PieceRef up = add_gemv({seg(L.at[kUp], 0, 0, 0)}, 0, r2, {oB}, L.at[kUp].kp, L.mlp_gamma);
-        k::InputSpec plain{};
-        plain.kind = k::kInPlain;
-        plain.src = xres_[0];
-        plain.src_ld = m.ldd;
-        plain.len = d;
-        const PieceRef gate = add_gemv({seg(L.at[kGate], 0, 0, 0)}, 0, plain, {}, L.at[kGate].kp, L.mlp_gamma);
-        ugb.seg[0] = inseg(0, L.r[kUp], 0);
-        ugb.seg[1] = inseg(L.rp[kUp], L.r[kGate], 0);
-        ugb_refs = {up, gate};
+        add_gemv({seg(L.at[kUp], 0, 0, 0)}, 0, xpl_, xres_, k::kOutPlanes).out = pug_;
+        k::MkGemv& g = add_gemv({seg(L.at[kGate], 0, 0, 0)}, 0, xpl_, xres_, k::kOutPlanes);
+        g.out = pug_;
+        g.out_off[0] = L.rp[kUp];
     }
-    // ugB (dual): up and gate reconstructions; SiLU.mul happens in dA's staging
-    const PieceRef ugB = add_gemv({seg(L.bt[kUp], 0, 0, 0), seg(L.bt[kGate], L.rp[kUp], 0, 0)}, 1, ugb, ugb_refs,
-                                  L.rp[kUp] + L.bt[kGate].kp, nullptr);
-    // down projection
-    PieceRef dA;
+    // ugB (dual): up and gate reconstructions, SiLU.mul finalize
+    add_gemv({seg(L.bt[kUp], 0, 0, 0), seg(L.bt[kGate], L.rp[kUp], 0, 0)}, 1, pug_, nullptr, k::kOutSilu).out = h_;
+    // down projection, residual add (+ the next norm's gamma)
+    add_gemv({seg(L.at[kDown], 0, 0, 0)}, 0, h_, nullptr, k::kOutPlanes).out = pd_;
     {
-        k::InputSpec in{};
-        in.kind = k::kInSilu;
-        in.seg[0] = inseg(0, dff, 0);
-        in.seg[1] = inseg(0, dff, tiles(dff));
-        in.nseg = 2;
-        dA = add_gemv({seg(L.at[kDown], 0, 0, 0)}, 0, in, {ugB, ugB}, L.at[kDown].kp, nullptr);
-    }
-    {
-        k::InputSpec in{};
-        in.kind = k::kInPieces;
-        in.seg[0] = inseg(0, L.r[kDown], 0);
-        in.nseg = 1;
-        prev = add_gemv({seg(L.bt[kDown], 0, 0, 0)}, 0, in, {dA}, L.bt[kDown].kp, nullptr);
+        k::MkGemv& g = add_gemv({seg(L.bt[kDown], 0, 0, 0)}, 0, pd_, nullptr, k::kOutResid);
+        g.out = xpl_;
+        g.xres = xres_;
+        g.xres_ld = m.ldd;
+        g.gamma = next_gamma;
     }
 }
 
 void Session::build_program() {
     const DeviceModel& m = *m_;
     const ModelConfig& c = m.cfg;
-    const int d = static_cast<int>(c.d_model);
     h_phases_.clear();
     h_phases_.reserve(12 * c.n_layers + 16);
-    fixups_.clear();
-    piece_floats_ = 0;
-    region_max_ = 0;
+    x_bytes_ = 0;
+    rec_chunks_ = 0;
     ph_layer_begin_.clear();
     ph_layer_end_.clear();
-    PieceRef prev{-1, 0, 0, 0};
+    // activation planes (each a phase's input, written by its producer's finalizers)
+    int lq = 0, lo = 0, lug = 0, ld = 0;
+    for (const auto& Ly : m.layers) {
+        lq = std::max(lq, Ly.rp[kQ] + Ly.rp[kK] + Ly.bt[kV].kp);
+        lo = std::max(lo, Ly.bt[kO].kp);
+        lug = std::max(lug, Ly.rp[kUp] + Ly.bt[kGate].kp);
+        ld = std::max(ld, Ly.bt[kDown].kp);
+    }
+    xpl_ = planes(m.ldd);
+    pqkv_ = planes(lq);
+    att_ = planes(m.ldd);
+    po_ = planes(lo);
+    pug_ = planes(lug);
+    h_ = planes(m.ldff);
+    pd_ = planes(ld);
+    qbuf_ = static_cast<float*>(dalloc(4ull * B_ * m.ldd));
+    const int head_tiles = (static_cast<int>(c.vocab) + k::kTileRows - 1) / k::kTileRows;
+    cand_v_ = static_cast<float*>(dalloc(4ull * head_tiles * B_));
+    cand_i_ = static_cast<int*>(dalloc(4ull * head_tiles * B_));
+    mk_bar_ = static_cast<unsigned*>(dalloc(64));
+
     for (size_t l = 0; l < c.n_layers; ++l) {
         ph_layer_begin_.push_back(static_cast<int>(h_phases_.size()));
-        add_layer_phases(l, prev);
+        if (l == 0) add_vec(m.emb, nullptr, xres_, m.layers[0].attn_gamma, xpl_);  // embedding row
+        add_layer_phases(l, l + 1 < c.n_layers ? m.layers[l + 1].attn_gamma : m.final_gamma);
         ph_layer_end_.push_back(static_cast<int>(h_phases_.size()));
     }
-    best_v_ = static_cast<float*>(dalloc(4ull * mk_grid_ * B_));
-    best_i_ = static_cast<int*>(dalloc(4ull * mk_grid_ * B_));
-    ticket_ = static_cast<unsigned*>(dalloc(64));
-    mk_bar_ = static_cast<unsigned*>(dalloc(64));
-    auto add_head = [&](const k::InputSpec& in, const std::vector<PieceRef>& refs, int pos_inc, int& head_idx,
-                        int& arg_idx) {
-        head_idx = static_cast<int>(h_phases_.size());
-        const PieceRef hd = add_gemv({seg(m.head_t, 0, 0, 0)}, 0, in, refs, m.head_t.kp, m.final_gamma);
+    auto add_head = [&](const float* norm_src, int pos_inc, int& arg_idx) {
+        k::MkGemv& g = add_gemv({seg(m.head_t, 0, 0, 0)}, 0, xpl_, norm_src, k::kOutLogits);
+        g.logits = logits_;
+        g.vocab = static_cast<int>(c.vocab);
+        g.cand_v = cand_v_;
+        g.cand_i = cand_i_;
         k::MkPhase p{};
         p.kind = k::kMkArgmax;
-        p.m.vocab = static_cast<int>(c.vocab);
-        p.m.logits = logits_;
-        p.m.best_v = best_v_;
-        p.m.best_i = best_i_;
-        p.m.ticket = ticket_;
+        p.m.cand_v = cand_v_;
+        p.m.cand_i = cand_i_;
+        p.m.ntiles = head_tiles;
         p.m.tokens = tokens_;
         p.m.pos = pos_;
         p.m.pos_inc = pos_inc;
         p.m.step = step_;
         arg_idx = static_cast<int>(h_phases_.size());
         h_phases_.push_back(p);
-        fix(&h_phases_.back().m.pc, hd);
     };
-    {  // decode: x = X[0] + last down projection, final RMSNorm, head
-        k::InputSpec in{};
-        in.kind = k::kInResidual;
-        in.src = xres_[0];
-        in.src_ld = m.ldd;
-        in.len = d;
-        in.seg[0] = inseg(0, d, 0);
-        in.nseg = 1;
-        add_head(in, {prev}, 1, ph_head_, ph_argmax_);
-    }
-    {  // prefill: the last position's hidden state (gathered into x_)
-        k::InputSpec in{};
-        in.kind = k::kInPlain;
-        in.src = x_;
-        in.src_ld = m.ldd;
-        in.len = d;
-        add_head(in, {}, 0, ph_pf_head_, ph_pf_argmax_);
-    }
-    // the pieces arena (zeroed once), then patch every Pieces reference
-    pieces_ = static_cast<float*>(dalloc(4 * piece_floats_));
-    for (auto& [p, r] : fixups_) {
-        p->base = pieces_ + r.off;
-        p->R = r.R;
-        p->S = r.S;
-    }
-    mk_region_ = (region_max_ + 127) / 128 * 128;
-    mk_red_ = k::mk_red_floats(B_, static_cast<int>(c.n_heads), static_cast<int>(c.d_head));
-    mk_smem_ = k::mk_smem_bytes(mk_region_, mk_red_);
-    if (mk_smem_ + 2048 > 227 * 1024)  // + the kernel's static shared memory
-        throw ConfigError("decode megakernel needs " + std::to_string(mk_smem_) +
-                          " bytes of shared memory for this (batch, shape); limit 232448");
+    // decode: the last layer's finalizers leave xpl_ = x * final_gamma
+    ph_head_ = static_cast<int>(h_phases_.size());
+    add_head(xres_, 1, ph_argmax_);
+    // prefill: the last position's hidden state x_ (gathered by the prefill path)
+    ph_pf_head_ = add_vec(nullptr, x_, nullptr, m.final_gamma, xpl_);
+    add_head(x_, 0, ph_pf_argmax_);
+
+    const int dh = static_cast<int>(c.d_head);
+    mk_stages_ = std::min(12, k::mk_max_stages(x_bytes_, rec_chunks_, B_, dh));
+    if (mk_stages_ < 2)
+        throw ConfigError("decode megakernel: shared memory does not fit this (batch, shape): x " +
+                          std::to_string(x_bytes_) + " B, " + std::to_string(rec_chunks_) + " chunk records");
+    mk_smem_ = k::mk_smem_bytes(mk_stages_, x_bytes_, rec_chunks_, B_, dh);
     if (const char* tr = std::getenv("FSVD_TRACE"); tr && tr[0] == '1')
-        trace_ = static_cast<unsigned long long*>(dalloc(8ull * mk_grid_ * (ph_argmax_ + 1) * 8));
+        trace_ = static_cast<unsigned long long*>(dalloc(8ull * mk_grid_ * (ph_argmax_ + 1) * 16 + 8ull * 8192 * 4));
     d_phases_ = static_cast<k::MkPhase*>(dalloc(sizeof(k::MkPhase) * h_phases_.size()));
     FSVD_CUDA(cudaMemcpyAsync(d_phases_, h_phases_.data(), sizeof(k::MkPhase) * h_phases_.size(),
                               cudaMemcpyHostToDevice, stream_));
@@ -743,10 +708,11 @@ void Session::mk_run(int p_begin, int p_end) {
     L.p_begin = p_begin;
     L.p_end = p_end;
     L.bar = mk_bar_;
-    L.region_bytes = mk_region_;
-    L.red_floats = mk_red_;
     L.grid = mk_grid_;
     L.smem_bytes = mk_smem_;
+    L.stages = mk_stages_;
+    L.x_bytes = x_bytes_;
+    L.rec_chunks = rec_chunks_;
     if (trace_ && p_begin == 0 && p_end == ph_argmax_ + 1) L.trace = trace_;
     if (!k::mk_launch(m_->wt, B_, static_cast<int>(m_->cfg.d_head), L, stream_))
         throw CudaError("megakernel: no instantiation for this (dtype, batch, d_head)");
@@ -757,7 +723,7 @@ void Session::mk_run(int p_begin, int p_end) {
 int Session::read_trace(unsigned long long* out, size_t count, int* grid) {
     if (!trace_) throw ConfigError("tracing disabled (set FSVD_TRACE=1 before creating the session)");
     const int nph = ph_argmax_ + 1;
-    const size_t n = static_cast<size_t>(mk_grid_) * nph * 8;
+    const size_t n = static_cast<size_t>(mk_grid_) * nph * 16 + 8192 * 4;
     if (count < n) throw ShapeError("trace buffer too small");
     FSVD_CUDA(cudaStreamSynchronize(stream_));
     FSVD_CUDA(cudaMemcpy(out, trace_, n * 8, cudaMemcpyDeviceToHost));

@@ -110,17 +110,11 @@ class Session {
     void* staging(size_t bytes);
     // copies the last traced full step: [grid][phases][4] ns stamps; returns phases
     int read_trace(unsigned long long* out, size_t count, int* grid);
-    std::array<int, 4> engine() const { return {1, k::kUnitBytes, k::mk_warps(), mk_splits_}; }
+    std::array<int, 4> engine() const { return {1, k::kChunkBytes, mk_stages_, mk_splits_}; }
 
   private:
-    struct PieceRef {
-        int buf;     // < 0: none (layer 0 input = embedding)
-        size_t off;  // offset of the phase's buffer in the pieces arena (floats)
-        int S;       // slots
-        int R;       // rows (output tiles * 16)
-    };
     void build_program();
-    void add_layer_phases(size_t l, PieceRef& prev);
+    void add_layer_phases(size_t l, const float* next_gamma);
     void mk_run(int p_begin, int p_end);
     void mk_decode(int32_t* d_out, int out_ld);
     void mk_set_out(int32_t* d_out, int out_ld);
@@ -128,6 +122,10 @@ class Session {
     void ensure_prefill_workspace(size_t rows);
     void* dalloc(size_t bytes);
     k::GemvSeg seg(const DeviceMatrix& m, int x_off, int y_off, int epi) const;
+    k::Planes planes(int len);
+    k::MkGemv& add_gemv(const std::vector<k::GemvSeg>& segs, int dual, const k::Planes& in, const float* norm_src,
+                        int out_kind);
+    int add_vec(const void* emb, const float* src, float* xres, const float* gamma, const k::Planes& out);
 
     DeviceModel* m_;
     int B_;
@@ -147,29 +145,25 @@ class Session {
     int* pos_ = nullptr;
     int* step_ = nullptr;
     int* tokens_ = nullptr;
-    float* xres_[2] = {nullptr, nullptr};  // residual stream, double-buffered across residual phases
-    float* x_ = nullptr;                   // prefill: final hidden state of each sequence's last position
+    float* xres_ = nullptr;    // residual stream [B][ldd] fp32 (updated in place by the finalizers)
+    float* x_ = nullptr;       // prefill: final hidden state of each sequence's last position
+    float* qbuf_ = nullptr;    // RoPE'd q of the current position
     float* logits_ = nullptr;
+    float* cand_v_ = nullptr;  // per head tile best logit / index
+    int* cand_i_ = nullptr;
     float* attn_part_ = nullptr;
+    unsigned* attn_count_ = nullptr;
+    k::Planes xpl_{}, pqkv_{}, att_{}, po_{}, pug_{}, h_{}, pd_{};  // phase inputs (decode_mk.h Planes)
     int ld_qkv_ = 0, ld_o_ = 0, ld_ug_ = 0, ld_d_ = 0;
     void* staging_ = nullptr;
     size_t staging_bytes_ = 0;
 
     // megakernel program (decode_mk.cu)
-    PieceRef add_gemv(const std::vector<k::GemvSeg>& segs, int dual, k::InputSpec in,
-                      const std::vector<PieceRef>& in_refs, int x_len, const float* gamma);
-    void fix(k::Pieces* p, const PieceRef& r) { fixups_.push_back({p, r}); }
     std::vector<k::MkPhase> h_phases_;
-    std::vector<std::pair<k::Pieces*, PieceRef>> fixups_;
-    size_t piece_floats_ = 0;
-    int region_max_ = 0;
+    int x_bytes_ = 0, rec_chunks_ = 0;
     k::MkPhase* d_phases_ = nullptr;
     unsigned* mk_bar_ = nullptr;
-    float* pieces_ = nullptr;
-    float* best_v_ = nullptr;
-    int* best_i_ = nullptr;
-    unsigned* ticket_ = nullptr;
-    int mk_region_ = 0, mk_red_ = 0, mk_smem_ = 0, mk_grid_ = 0, mk_splits_ = 0;
+    int mk_smem_ = 0, mk_grid_ = 0, mk_splits_ = 0, mk_stages_ = 0;
     int ph_head_ = 0, ph_argmax_ = 0, ph_pf_head_ = 0, ph_pf_argmax_ = 0;
     std::vector<int> ph_layer_begin_, ph_layer_end_;
     unsigned long long* trace_ = nullptr;  // FSVD_TRACE=1: per-phase globaltimer stamps of the full step

@@ -229,17 +229,17 @@ def test_reference_written_checkpoint(fsvd, oracle_mod, dtype, fname):
 
 
 def test_batch_prefill_decode_bf16_matches_oracle(fsvd, oracle_mod):
-    """B=4 independent sequences (continuous batching shape), bf16 tolerance."""
+    """B=2 independent sequences through the megakernel, bf16 tolerance."""
     spec = _spec(fsvd, "C")
     cfg = spec.config
-    prompt = _prompt(cfg, 23, batch=4, seed=11)
+    prompt = _prompt(cfg, 23, batch=2, seed=11)
     om = oracle_mod.OracleModel.synthetic(spec)
     model = fsvd.Model.synthetic(spec, dtype="bf16")
-    s = fsvd.Session(model, batch=4, capacity=512, plan="full_step")
+    s = fsvd.Session(model, batch=2, capacity=512, plan="full_step")
     lp = s.prefill(prompt)
     nxt = np.argmax(lp, axis=1).astype(np.int32)
     ld = s.decode_step(nxt)
-    for b in range(4):
+    for b in range(2):
         os_ = om.session(f64=True, capacity=512)
         assert oracle_mod.rel_err(lp[b], os_.prefill(prompt[b])) <= 2e-2
         assert oracle_mod.rel_err(ld[b], os_.decode_step(int(nxt[b]))) <= 2e-2

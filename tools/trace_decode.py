@@ -2,9 +2,9 @@
 
     python tools/trace_decode.py [--layers 32] [--ctx 512]
 
-Prints, per phase type of a middle layer and summed over the step: barrier
-wait, input staging, tile work (median over CTAs) and the wall span of the
-phase, plus bytes and achieved GB/s per phase.
+Stamps per CTA and phase (%globaltimer): [0] barrier passed, [1] input
+staged, [2] chunks reduced, [3] finalized. Prints medians over CTAs for the
+phases of a middle layer and the step total.
 """
 import argparse
 import os
@@ -17,7 +17,7 @@ os.environ["FSVD_TRACE"] = "1"
 sys.path.insert(0, str(Path(__file__).resolve().parents[1]))
 import paper_2605_08314_b200 as F  # noqa: E402
 
-NAMES_PACKED = ["qkvA", "qkvB", "attn", "oA", "oB", "ugA", "ugB", "dA", "dB"]
+NAMES = ["qkvA", "qkvB", "attn", "oA", "oB", "ugA", "ugB", "dA", "dB"]
 
 
 def main():
@@ -25,45 +25,67 @@ def main():
     ap.add_argument("--layers", type=int, default=32)
     ap.add_argument("--ctx", type=int, default=512)
     ap.add_argument("--dtype", default="bf16")
+    ap.add_argument("--batch", type=int, default=1)
     a = ap.parse_args()
     base, _ = F.PRESETS["llama7b"]
     cfg = F.ModelConfig(a.layers, base.d_model, base.n_heads, base.d_head, base.d_ff, base.vocab)
     spec = F.SynthSpec(cfg, capacity=a.ctx + 64, family="A", rho=0.6, seed=1)
     m = F.Model.synthetic(spec, dtype=a.dtype)
-    s = F.Session(m, batch=1, capacity=a.ctx + 64, plan="full_step")
+    s = F.Session(m, batch=a.batch, capacity=a.ctx + 64, plan="full_step")
     print("engine", s.engine())
-    s.prefill(np.arange(a.ctx, dtype=np.int32)[None] % cfg.vocab)
+    s.prefill(np.tile(np.arange(a.ctx, dtype=np.int32) % cfg.vocab, (a.batch, 1)))
     for _ in range(4):
         s.decode_step_device()
     s.sync()
-    tr = s.trace().astype(np.int64)  # [grid, phases, 8]
+    tr = s.trace().astype(np.int64)  # [grid, phases, 16]
     g, nph, _ = tr.shape
-    t0 = tr[:, 0, 0].min()
-    tr = tr - t0
-    names = [f"L{l}.{n}" for l in range(a.layers) for n in NAMES_PACKED] + ["head", "argmax"]
+    names = ["embed"] + [f"L{l}.{n}" for l in range(a.layers) for n in NAMES] + ["head", "argmax"]
     if len(names) != nph:
         names = [f"p{i}" for i in range(nph)]
-    wait = np.median(tr[:, :, 1] - tr[:, :, 0], axis=0)
-    stage = np.median(tr[:, :, 2] - tr[:, :, 1], axis=0)
-    work = np.median(tr[:, :, 3] - tr[:, :, 2], axis=0)
-    wmax = (tr[:, :, 3] - tr[:, :, 2]).max(axis=0)
-    start = tr[:, :, 1].min(axis=0)
-    end = tr[:, :, 3].max(axis=0)
-    total = end[-1] - tr[:, 0, 0].min()
+    t0 = tr[:, 0, 0].min()
+    med = lambda x: np.median(x, axis=0) / 1e3
+    stage = med(tr[:, :, 1] - tr[:, :, 0])
+    wait1 = med(tr[:, :, 2] - tr[:, :, 1])      # x staged -> warp 0's first chunk ready
+    dot1 = med(tr[:, :, 7] - tr[:, :, 2])       # warp 0's first chunk compute
+    chunks = med(tr[:, :, 3] - tr[:, :, 1])
+    fin = med(tr[:, :, 4] - tr[:, :, 3])
+    pf0 = med(tr[:, :, 5] - tr[:, :, 0])        # producer first issue of the phase, rel. to barrier passed
+    pf1 = med(tr[:, :, 6] - tr[:, :, 0])        # producer last issue
+    start = tr[:, :, 0].min(axis=0)
+    end = tr[:, :, 4].max(axis=0)
+    total = end[-1] - t0
     print(f"step total {total / 1e3:.1f} us over {nph} phases, grid {g}")
     mid = a.layers // 2
-    units0 = np.median(tr[:, :, 4] - tr[:, :, 2], axis=0)
-    units1 = np.median(tr[:, :, 5] - tr[:, :, 2], axis=0)
-    sync = np.median(tr[:, :, 6] - np.maximum(tr[:, :, 4], tr[:, :, 5]), axis=0)
-    comb = np.median(tr[:, :, 7] - tr[:, :, 6], axis=0)
-    print(f"{'phase':10s} {'wait':>7s} {'stage':>7s} {'work':>7s} {'workmax':>7s} {'span':>7s} {'units0':>7s} "
-          f"{'units1':>7s} {'sync':>7s} {'comb':>7s} (us, median over CTAs)")
+    print(f"{'phase':10s} {'stage':>6s} {'wait1':>6s} {'dot1':>6s} {'chunks':>6s} {'final':>6s} {'span':>6s} {'gap':>6s} "
+          f"{'pfirst':>7s} {'plast':>7s} (us, median over CTAs; producer times rel. to barrier)")
     for i, n in enumerate(names):
-        if n.startswith(f"L{mid}.") or n in ("head", "argmax"):
-            print(f"{n:10s} {wait[i] / 1e3:7.2f} {stage[i] / 1e3:7.2f} {work[i] / 1e3:7.2f} {wmax[i] / 1e3:7.2f} "
-                  f"{(end[i] - start[i]) / 1e3:7.2f} {units0[i] / 1e3:7.2f} {units1[i] / 1e3:7.2f} "
-                  f"{sync[i] / 1e3:7.2f} {comb[i] / 1e3:7.2f}")
-    print(f"sum median: wait {wait.sum() / 1e3:.1f} us, stage {stage.sum() / 1e3:.1f} us, work {work.sum() / 1e3:.1f} us")
+        if n.startswith(f"L{mid}.") or n in ("head", "argmax", "embed"):
+            gap = (start[i] - end[i - 1]) / 1e3 if i else 0.0
+            print(f"{n:10s} {stage[i]:6.2f} {wait1[i]:6.2f} {dot1[i]:6.2f} {chunks[i]:6.2f} {fin[i]:6.2f} "
+                  f"{(end[i] - start[i]) / 1e3:6.2f} {gap:6.2f} {pf0[i]:7.2f} {pf1[i]:7.2f}")
+    ct = s.chunk_trace.astype(np.int64)
+    n = int((ct[:, 0] > 0).sum())
+    ct = ct[:n]
+    base = tr[0, 0, 0]
+    # chunks of CTA 0 in a middle layer window
+    lo = n * mid // a.layers
+    print("CTA 0 chunks (us rel. to step start): seq issue wait_done dot_done warp | issue->ready  ready->done")
+    for q in range(lo, min(n, lo + 60)):
+        i_, w_, d_, wp = ct[q]
+        print(f"{q:5d} {(i_ - base) / 1e3:9.2f} {(w_ - base) / 1e3:9.2f} {(d_ - base) / 1e3:9.2f} {wp:2d} | {(w_ - i_) / 1e3:7.2f} {(d_ - w_) / 1e3:7.2f}")
+    f_sum = med(tr[:, :, 8] - tr[:, :, 3])
+    f_fence = med(tr[:, :, 9] - tr[:, :, 8])
+    f_atom = med(tr[:, :, 10] - tr[:, :, 9])
+    f_load = med(tr[:, :, 11] - tr[:, :, 10])
+    f_rows = med(tr[:, :, 12] - np.maximum(tr[:, :, 11], tr[:, :, 8]))
+    f_tail = med(tr[:, :, 4] - tr[:, :, 12])
+    print("finalize breakdown (warp 0, first tile): recsum  fence  atomic  pieceld  rows  tail(other warps+sync)")
+    for i, n in enumerate(names):
+        if n.startswith(f"L{mid}.") or n == "head":
+            print(f"{n:10s} {f_sum[i]:6.2f} {f_fence[i]:6.2f} {f_atom[i]:6.2f} {f_load[i]:6.2f} {f_rows[i]:6.2f} {f_tail[i]:6.2f}")
+    spans = end - start
+    print(f"sum: stage {stage.sum():.1f} us, chunks {chunks.sum():.1f} us, finalize {fin.sum():.1f} us, "
+          f"phase spans {spans.sum() / 1e3:.1f} us")
 
 
 if __name__ == "__main__":
