@@ -52,13 +52,29 @@ struct Smem {
     MkPhase* desc;     // [2] phase descriptors (double-buffered bulk copies)
     uint64_t* dbar;    // [2]
     void* gsh;         // GemvShared
+    MkChunk* meta;     // [stages] record of the chunk in each ring slot
+};
+
+// Per-phase shared state of a GEMV phase (computed once, read by all warps).
+struct GemvShared {
+    MkSplit sp;
+    int ulo, uhi, Tf;
+    unsigned cnt[kMkMaxLocalTiles];  // chunk completions per local tile (0x10000 = tile complete)
+    float inv[4];
+    unsigned next;                   // dynamic chunk assignment
+    int nchunks;                     // this CTA's chunks in the phase
+    unsigned released[16];           // rounds of each ring slot consumed so far (whole launch)
+    int pos;                         // length register, read once per launch
+    float2 rope[64];                 // kOutQKV: (cos, sin) of position pos
+    float xpf[8 * kTileRows * 4];    // kOutResid: residual rows of the CTA's tiles (<= 8 tiles)
 };
 
 // ---------------------------------------------------------------- GEMV ----
 template <typename W, int B>
-__device__ __forceinline__ void finalize_rows(const MkGemv& g, const MkSplit& sp, int T, int i, const float (&v)[2][B],
-                                              const float* inv) {
+__device__ __forceinline__ void finalize_rows(const MkGemv& g, const GemvShared& sh, int T, int i,
+                                              const float (&v)[2][B], const float* inv) {
     using IO = PlaneIO<W>;
+    const MkSplit& sp = sh.sp;
     // segment and row of output tile T
     int s = 0;
     if (!sp.dual)
@@ -76,7 +92,9 @@ __device__ __forceinline__ void finalize_rows(const MkGemv& g, const MkSplit& sp
 #pragma unroll
                 for (int b = 0; b < B; ++b) {
                     float* xr = g.xres + static_cast<size_t>(b) * g.xres_ld + row;
-                    const float x = __ldcg(xr) + v[0][b];
+                    const int pr = row - sh.Tf * kTileRows;  // prefetched residual rows of this CTA
+                    const float x0 = pr < 8 * kTileRows ? sh.xpf[pr * B + b] : __ldcg(xr);
+                    const float x = x0 + v[0][b];
                     *xr = x;
                     IO::put(g.out, b, row, x * g.gamma[row]);
                 }
@@ -115,7 +133,7 @@ __device__ __forceinline__ void finalize_rows(const MkGemv& g, const MkSplit& sp
             break;
         }
         default: {  // kOutQKV: segment 0 q, 1 k, 2 v
-            const int pos = *g.pos;
+            const int pos = sh.pos;
             float o[B];
 #pragma unroll
             for (int b = 0; b < B; ++b) {
@@ -124,7 +142,7 @@ __device__ __forceinline__ void finalize_rows(const MkGemv& g, const MkSplit& sp
                 o[b] = x;
                 if (s < 2) {
                     const int e = row % g.d_head;
-                    const float2 cs = g.rope[static_cast<long long>(pos) * (g.d_head / 2) + (e >> 1)];
+                    const float2 cs = sh.rope[e >> 1];
                     const float x0 = (e & 1) ? y : x, x1 = (e & 1) ? x : y;
                     o[b] = (e & 1) ? __fadd_rn(__fmul_rn(x0, cs.y), __fmul_rn(x1, cs.x))
                                    : __fsub_rn(__fmul_rn(x0, cs.x), __fmul_rn(x1, cs.y));
@@ -210,21 +228,14 @@ __device__ __forceinline__ bool exchange_pieces(const MkGemv& g, const MkSplit& 
     return true;
 }
 
-// Per-phase shared state of a GEMV phase (computed once, read by all warps).
-struct GemvShared {
-    MkSplit sp;
-    int ulo, uhi, Tf;
-    unsigned cnt[kMkMaxLocalTiles];  // chunk completions per local tile (0x10000 = tile complete)
-    float inv[4];
-    unsigned next;                   // dynamic chunk assignment
-};
-
 template <typename W, int B>
 __device__ void gemv_phase(const MkGemv& g, const Smem& sm, GemvShared& sh, int tid, int cta, int G, uint32_t& cseq,
-                           uint32_t& xphase, int stages, unsigned long long* tr, unsigned long long* ctr) {
+                           uint32_t& xphase, int stages, unsigned long long* tr, unsigned long long* ctr, int chunk_lo,
+                           int chunk_hi, volatile int* prog) {
     constexpr int ES = sizeof(W);
     const int warp = tid >> 5, lane = tid & 31;
-    // ---- stage the input planes (one bulk copy), split, RMSNorm scale ----
+    // ---- stage the input planes (one bulk copy), split, RMSNorm scale,
+    // finalize operands -- all loads in flight together ----
     if (tid == 0) {
         const uint32_t xbytes = static_cast<uint32_t>(B) * g.in.len * PlaneIO<W>::kBytesPerElem;
         fence_proxy_async_global();
@@ -235,6 +246,7 @@ __device__ void gemv_phase(const MkGemv& g, const Smem& sm, GemvShared& sh, int 
         sh.uhi = sh.sp.lo(cta + 1, G);
         sh.Tf = sh.ulo < sh.uhi ? sh.sp.tile_of(sh.ulo) : 0;
         sh.next = 0u;
+        sh.nchunks = chunk_hi - chunk_lo;
     }
     if (tid < kMkMaxLocalTiles) sh.cnt[tid] = 0u;
     const int rec_per_tile = (g.rec_c0 + g.rec_c1) * kTileRows * B;
@@ -242,6 +254,17 @@ __device__ void gemv_phase(const MkGemv& g, const Smem& sm, GemvShared& sh, int 
         float4* r4 = reinterpret_cast<float4*>(sm.rec);
         const int n4 = g.rec_ntl * rec_per_tile / 4;
         for (int q = tid; q < n4; q += kConsumerThreads) r4[q] = make_float4(0.f, 0.f, 0.f, 0.f);
+    }
+    consumer_sync();
+    if (g.out_kind == kOutQKV && tid < g.d_head / 2)
+        sh.rope[tid] = g.rope[static_cast<long long>(sh.pos) * (g.d_head / 2) + tid];
+    if (g.out_kind == kOutResid && sh.ulo < sh.uhi) {
+        const int r0 = sh.Tf * kTileRows, nr = (sh.sp.tile_of(sh.uhi - 1) - sh.Tf + 1) * kTileRows;
+        if (nr <= 8 * kTileRows)
+            for (int q = tid; q < nr * B; q += kConsumerThreads) {
+                const int b = q / nr, r = q - b * nr;
+                sh.xpf[r * B + b] = r0 + r < g.seg[0].rows ? __ldcg(g.xres + static_cast<size_t>(b) * g.xres_ld + r0 + r) : 0.f;
+            }
     }
     if (g.norm_src) {
         float ss[B];
@@ -274,7 +297,9 @@ __device__ void gemv_phase(const MkGemv& g, const Smem& sm, GemvShared& sh, int 
     float inv[B];
 #pragma unroll
     for (int b = 0; b < B; ++b) inv[b] = sh.inv[b];
+    if (prog && tid == 0) prog[1] = 10;
     mbar_wait(sm.xbar, xphase & 1u);
+    if (prog && tid == 0) prog[1] = 11;
     ++xphase;
     if (tr && tid == 0) tr[1] = gtimer();
 
@@ -282,36 +307,34 @@ __device__ void gemv_phase(const MkGemv& g, const Smem& sm, GemvShared& sh, int 
     // completes a tile's last chunk finalizes the tile right away ----
     const W* xs = static_cast<const W*>(sm.x);
     const int c_stride[2] = {0, g.rec_c0};
-    ChunkSeq seq;
-    seq.begin(sp, sh.ulo, sh.uhi);
-    int T_prev = -1, c_tile = 0, pos = 0;
     const uint32_t cbase = cseq;
+    const int nchunks = sh.nchunks;
+    const uint4* meta = reinterpret_cast<const uint4*>(sm.meta);
     for (;;) {
-        // grab the next chunk (dynamic: a warp held up by a tile exchange never stalls the ring)
+        // grab the next chunk (dynamic: a warp held up never stalls the ring)
         int jn = 0;
         if (lane == 0) jn = static_cast<int>(atomicAdd(&sh.next, 1u));
         jn = __shfl_sync(0xffffffffu, jn, 0);
-        int nl = 0, s = 0, line = 0, T = 0, sub = 0, c = 0;
-        while (pos <= jn && !seq.done()) {  // walk to chunk jn (every chunk is visited once per warp)
-            nl = seq.it.lines(sp);
-            s = seq.it.s;
-            line = seq.it.line;
-            T = seq.tile(sp);
-            sub = seq.sub(sp);
-            c = seq.c_run;
-            c_tile = T == T_prev ? c_tile + 1 : 0;  // chunk index inside the output tile
-            T_prev = T;
-            seq.advance(sp, nl);
-            ++pos;
-        }
-        if (pos <= jn) break;  // past the last chunk
+        if (jn >= nchunks) break;
         const uint32_t cs = cbase + static_cast<uint32_t>(jn);
-        const bool last_of_tile = seq.done() || seq.tile(sp) != T;
-        const int k = T - sh.Tf;
-        const uint32_t slot = cs % stages, par = (cs / stages) & 1u;
+        const uint32_t slot = cs % stages, round = cs / stages, par = round & 1u;
+        if (prog && lane == 0) { prog[2 + warp] = 100000000 + static_cast<int>(cs); prog[10] = static_cast<int>(cbase); prog[11] = nchunks; }
+        // Chunks are grabbed dynamically, so two warps may want the same slot
+        // for consecutive rounds; the parity wait can only tell the current
+        // round from the previous one. Wait until the slot's previous round
+        // is consumed first, then the parity is unambiguous.
+        if (lane == 0)
+            while (*reinterpret_cast<volatile unsigned*>(&sh.released[slot]) != round) {
+            }
+        __syncwarp();
         mbar_wait(&sm.full[slot], par);
+        if (prog && lane == 0) prog[2 + warp] = 200000000 + static_cast<int>(cs);
         const unsigned long long t_wait = ctr ? gtimer() : 0ull;
-        const int kbase = g.seg[s].x_off + line * (kLineBytes / ES);
+        const uint4 mr = meta[slot];
+        const MkChunk& ch = *reinterpret_cast<const MkChunk*>(&mr);
+        const int nl = ch.nl & 0xF, sub = (ch.nl >> 4) & 1, T = ch.T, k = ch.k, c = ch.c, c_tile = ch.ctile;
+        const bool last_of_tile = (ch.nl & 0x20) != 0;
+        const int kbase = ch.kbase;
         float* rec = sm.rec + k * rec_per_tile + (c_stride[sub] + c) * kTileRows * B;
         ChunkDot<W, B>::run(sm.ring + static_cast<size_t>(slot) * kChunkBytes, nl, xs, g.in.len, kbase, lane, rec);
         __syncwarp();
@@ -322,6 +345,7 @@ __device__ void gemv_phase(const MkGemv& g, const Smem& sm, GemvShared& sh, int 
         }
         unsigned done = 0;
         if (lane == 0) {
+            *reinterpret_cast<volatile unsigned*>(&sh.released[slot]) = round + 1u;
             mbar_arrive(&sm.empty[slot]);
             __threadfence_block();
             // every chunk adds 1; the tile's last chunk adds 0x10000 - c_tile, so the
@@ -347,9 +371,10 @@ __device__ void gemv_phase(const MkGemv& g, const Smem& sm, GemvShared& sh, int 
                 v[sb][b] = acc;
             }
         if (!exchange_pieces<B>(g, sp, T, cta, G, lane, v)) continue;
-        finalize_rows<W, B>(g, sp, T, lane, v, inv);
+        finalize_rows<W, B>(g, sh, T, lane, v, inv);
     }
-    cseq = cbase + static_cast<uint32_t>(pos);  // every warp walked all chunks of the phase
+    if (prog && lane == 0) prog[2 + warp] = 3000000 + nchunks;
+    cseq = cbase + static_cast<uint32_t>(nchunks);
     consumer_sync();
     if (tr && tid == 0) tr[3] = gtimer();
 }
@@ -376,10 +401,10 @@ __device__ __forceinline__ void load_kv_row(const T* p, float* out) {
 }
 
 template <typename W, int B, int DH>
-__device__ void attn_phase(const MkAttn& a, const Smem& sm, int tid, int cta, int G) {
+__device__ void attn_phase(const MkAttn& a, const Smem& sm, int tid, int cta, int G, int pos) {
     constexpr int PER = DH / 32, KU = 8, ST = DH + 2;
     const int warp = tid >> 5, lane = tid & 31;
-    const int pos = *a.pos, len = pos + 1;
+    const int len = pos + 1;
     RowSplit rs{B * a.n_heads * len};
     const int r0 = rs.lo(cta, G), r1 = rs.lo(cta + 1, G);
     float* wst = sm.rec;  // [warps][DH + 2]: acc, l, m
@@ -582,6 +607,7 @@ __global__ void __launch_bounds__(kThreads, 1) decode_mk_kernel(const __grid_con
     sm.desc = reinterpret_cast<MkPhase*>(sm.misc + 256);
     sm.dbar = reinterpret_cast<uint64_t*>(sm.desc + 2);
     sm.gsh = sm.dbar + 2;
+    sm.meta = reinterpret_cast<MkChunk*>(static_cast<char*>(sm.gsh) + (sizeof(GemvShared) + 15) / 16 * 16);
 
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31, cta = blockIdx.x, G = gridDim.x;
     if (tid == 0) {
@@ -598,43 +624,46 @@ __global__ void __launch_bounds__(kThreads, 1) decode_mk_kernel(const __grid_con
 
     if (warp == kConsumerWarps) {
         // ================= producer: weight stream of every GEMV phase =================
-        if (lane != 0) return;
-        constexpr int ES = sizeof(W);
+        // Walks this CTA's precomputed chunk records (host-built, in the
+        // consumers' order), 32 at a time: lane i loads record i of the batch,
+        // lane 0 issues them; the only wait is for a free ring slot.
         const uint64_t policy = evict_first_policy();
+        const int* st = L.chunk_start + static_cast<size_t>(cta) * (L.nphases + 1);
+        const int i0 = st[L.p_begin], i1 = st[L.p_end];
+        if (L.progress && lane == 0) {
+            L.progress[cta * 16 + 14] = i0;
+            L.progress[cta * 16 + 15] = i1;
+        }
+        uint4* meta = reinterpret_cast<uint4*>(sm.meta);
         uint32_t seq = 0;
-        for (int p = L.p_begin; p < L.p_end; ++p) {
-            const MkPhase& ph = L.phases[p];
-            if (ph.kind != kMkGemv) continue;
-            unsigned long long* tr =
-                L.trace ? L.trace + (static_cast<size_t>(cta) * (L.p_end - L.p_begin) + (p - L.p_begin)) * 16 : nullptr;
-            bool first = true;
-            const MkGemv& g = ph.g;
-            MkSplit sp;
-            sp.init(g.seg, g.nseg, g.dual, ES);
-            const char* wbase[3];
-            size_t tbytes[3];
-            for (int q = 0; q < 3; ++q) {
-                wbase[q] = static_cast<const char*>(g.seg[q].w);
-                tbytes[q] = g.seg[q].layout(ES).tile_bytes();
+        for (int ib = i0; ib < i1; ib += 32) {
+            uint4 rec = make_uint4(0u, 0u, 0u, 0u);
+            if (ib + lane < i1) rec = __ldg(reinterpret_cast<const uint4*>(L.chunks + ib + lane));
+            if (L.l2_ahead > 0 && ib + L.l2_ahead + lane < i1) {
+                const MkChunk ahead = L.chunks[ib + L.l2_ahead + lane];
+                prefetch_l2_bulk(ahead.src, static_cast<uint32_t>(ahead.nl & 0xF) * kLineTileBytes);
             }
-            ChunkSeq cs;
-            cs.begin(sp, sp.lo(cta, G), sp.lo(cta + 1, G));
-            for (; !cs.done(); ++seq) {
-                const int nl = cs.it.lines(sp);
-                const uint32_t bytes = static_cast<uint32_t>(nl) * kLineTileBytes;
-                const char* src = wbase[cs.it.s] + static_cast<size_t>(cs.it.t) * tbytes[cs.it.s] +
-                                  static_cast<size_t>(cs.it.line) * kLineTileBytes;
-                cs.advance(sp, nl);
-                const uint32_t slot = seq % L.stages;
-                mbar_wait(&sm.empty[slot], ((seq / L.stages) & 1u) ^ 1u);
-                mbar_expect_tx(&sm.full[slot], bytes);
-                bulk_g2s(sm.ring + static_cast<size_t>(slot) * kChunkBytes, src, bytes, &sm.full[slot], policy);
-                if (tr) {
-                    if (cta == 0 && seq < 8192) L.trace[static_cast<size_t>(G) * (L.p_end - L.p_begin) * 16 + seq * 4] = gtimer();
-                    if (first) tr[5] = gtimer();
-                    tr[6] = gtimer();
-                    first = false;
+            const int n = min(32, i1 - ib);
+            for (int q = 0; q < n; ++q, ++seq) {
+                uint4 r;
+                r.x = __shfl_sync(0xffffffffu, rec.x, q);
+                r.y = __shfl_sync(0xffffffffu, rec.y, q);
+                r.z = __shfl_sync(0xffffffffu, rec.z, q);
+                r.w = __shfl_sync(0xffffffffu, rec.w, q);
+                if (lane == 0) {
+                    const MkChunk& ch = *reinterpret_cast<const MkChunk*>(&r);
+                    const uint32_t slot = seq % L.stages;
+                    const uint32_t bytes = static_cast<uint32_t>(ch.nl & 0xF) * kLineTileBytes;
+                    if (L.progress) L.progress[cta * 16 + 12] = static_cast<int>(seq);
+                    mbar_wait(&sm.empty[slot], ((seq / L.stages) & 1u) ^ 1u);
+                    if (L.progress) L.progress[cta * 16 + 13] = static_cast<int>(seq);
+                    meta[slot] = r;
+                    mbar_expect_tx(&sm.full[slot], bytes);
+                    bulk_g2s(sm.ring + static_cast<size_t>(slot) * kChunkBytes, ch.src, bytes, &sm.full[slot], policy);
+                    if (L.trace && cta == 0 && seq < 8192)
+                        L.trace[static_cast<size_t>(G) * (L.p_end - L.p_begin) * 16 + seq * 4] = gtimer();
                 }
+                __syncwarp();
             }
         }
         return;
@@ -647,11 +676,19 @@ __global__ void __launch_bounds__(kThreads, 1) decode_mk_kernel(const __grid_con
         bulk_g2s_plain(&sm.desc[0], &L.phases[L.p_begin], kDescBytes, &sm.dbar[0]);
     }
     GemvShared& gsh = *static_cast<GemvShared*>(sm.gsh);
+    if (tid < 16) gsh.released[tid] = 0u;
+    const int* cst = L.chunk_start + static_cast<size_t>(cta) * (L.nphases + 1);
+    if (tid == 0) gsh.pos = L.pos ? __ldcg(L.pos) : 0;  // constant until the argmax phase (last of a step)
+    consumer_sync();
     uint32_t cseq = 0, xphase = 0;
     const int nph = L.p_end - L.p_begin;
     for (int p = L.p_begin; p < L.p_end; ++p) {
         const int idx = p - L.p_begin, buf = idx & 1;
         unsigned long long* tr = L.trace ? L.trace + (static_cast<size_t>(cta) * nph + idx) * 16 : nullptr;
+        if (L.progress && tid == 0) {
+            L.progress[cta * 16] = p;
+            L.progress[cta * 16 + 1] = 0;
+        }
         if (idx > 0) {  // grid barrier: every CTA finished phase idx-1
             if (tid == 0) {
                 const unsigned target = static_cast<unsigned>(idx) * G;
@@ -666,15 +703,19 @@ __global__ void __launch_bounds__(kThreads, 1) decode_mk_kernel(const __grid_con
             bulk_g2s_plain(&sm.desc[buf ^ 1], &L.phases[p + 1], kDescBytes, &sm.dbar[buf ^ 1]);
         }
         if (tr && tid == 0) for (int q = 0; q < 16; ++q) if (q != 5 && q != 6) tr[q] = gtimer();
+        if (L.progress && tid == 0) L.progress[cta * 16 + 1] = 1;
         mbar_wait(&sm.dbar[buf], (idx >> 1) & 1u);
+        if (L.progress && tid == 0) L.progress[cta * 16 + 1] = 2;
         const MkPhase& ph = sm.desc[buf];
         switch (ph.kind) {
-            case kMkGemv: gemv_phase<W, B>(ph.g, sm, gsh, tid, cta, G, cseq, xphase, L.stages, tr, tr && cta == 0 ? L.trace + static_cast<size_t>(G) * nph * 16 : nullptr); break;
-            case kMkAttn: attn_phase<W, B, DH>(ph.a, sm, tid, cta, G); break;
+            case kMkGemv: gemv_phase<W, B>(ph.g, sm, gsh, tid, cta, G, cseq, xphase, L.stages, tr, tr && cta == 0 ? L.trace + static_cast<size_t>(G) * nph * 16 : nullptr, cst[p], cst[p + 1], L.progress ? L.progress + cta * 16 : nullptr); break;
+            case kMkAttn: attn_phase<W, B, DH>(ph.a, sm, tid, cta, G, gsh.pos); break;
             case kMkArgmax: argmax_phase<B>(ph.m, sm, tid, cta); break;
             default: vec_phase<W, B>(ph.v, tid, cta, G); break;
         }
+        if (L.progress && tid == 0) L.progress[cta * 16 + 1] = 3;
         consumer_sync();
+        if (L.progress && tid == 0) L.progress[cta * 16 + 1] = 4;
         if (tr && tid == 0) tr[4] = gtimer();
         if (tid == 0) {  // arrive (release): this CTA's writes of phase idx are complete
             if (idx + 1 < nph) {
@@ -747,13 +788,61 @@ void mk_split_stats(const GemvSeg* seg, int nseg, int dual, int esize, int grid,
     *rec_c1 = c1;
 }
 
+void mk_build_chunks(const MkPhase* phases, int nphases, int grid, int esize, std::vector<MkChunk>& out,
+                     std::vector<int>& start) {
+    out.clear();
+    start.assign(static_cast<size_t>(grid) * (nphases + 1), 0);
+    for (int c = 0; c < grid; ++c) {
+        for (int p = 0; p < nphases; ++p) {
+            start[static_cast<size_t>(c) * (nphases + 1) + p] = static_cast<int>(out.size());
+            if (phases[p].kind != kMkGemv) continue;
+            const MkGemv& g = phases[p].g;
+            MkSplit sp;
+            sp.init(g.seg, g.nseg, g.dual, esize);
+            const int ulo = sp.lo(c, grid), uhi = sp.lo(c + 1, grid);
+            if (ulo >= uhi) continue;
+            const int Tf = sp.tile_of(ulo);
+            ChunkSeq cs;
+            cs.begin(sp, ulo, uhi);
+            int T_prev = -1, ctile = 0;
+            const size_t first = out.size();
+            while (!cs.done()) {
+                MkChunk ch{};
+                const int nl = cs.it.lines(sp), s = cs.it.s;
+                const int T = cs.tile(sp);
+                ctile = T == T_prev ? ctile + 1 : 0;
+                T_prev = T;
+                const WLayout lay = g.seg[s].layout(esize);
+                ch.src = static_cast<const char*>(g.seg[s].w) + static_cast<size_t>(cs.it.t) * lay.tile_bytes() +
+                         static_cast<size_t>(cs.it.line) * kLineTileBytes;
+                const int kbase = g.seg[s].x_off + cs.it.line * (kLineBytes / esize);
+                if (T > 0xFFFF || kbase > 0xFFFF || T - Tf > 255 || cs.c_run > 255 || ctile > 255)
+                    throw std::runtime_error("decode megakernel: chunk record field overflow");
+                ch.T = static_cast<uint16_t>(T);
+                ch.kbase = static_cast<uint16_t>(kbase);
+                ch.nl = static_cast<uint8_t>(nl | (cs.sub(sp) ? 0x10 : 0));
+                ch.k = static_cast<uint8_t>(T - Tf);
+                ch.c = static_cast<uint8_t>(cs.c_run);
+                ch.ctile = static_cast<uint8_t>(ctile);
+                cs.advance(sp, nl);
+                out.push_back(ch);
+            }
+            // mark the last chunk of every output tile
+            for (size_t i = first; i < out.size(); ++i)
+                if (i + 1 == out.size() || out[i + 1].T != out[i].T) out[i].nl |= 0x20;
+        }
+        start[static_cast<size_t>(c) * (nphases + 1) + nphases] = static_cast<int>(out.size());
+    }
+}
+
 static int rec_floats(int rec_chunks, int batch, int d_head) {
     return std::max(rec_chunks * kTileRows * batch, mk::kConsumerWarps * (d_head + 2));
 }
 
 int mk_smem_bytes(int stages, int x_bytes, int rec_chunks, int batch, int d_head) {
     return stages * kChunkBytes + mk::mk_barrier_bytes(stages) + x_bytes + rec_floats(rec_chunks, batch, d_head) * 4 +
-           256 * 4 + 2 * static_cast<int>(sizeof(MkPhase)) + 16 + static_cast<int>(sizeof(mk::GemvShared)) + 16;
+           256 * 4 + 2 * static_cast<int>(sizeof(MkPhase)) + 16 + static_cast<int>(sizeof(mk::GemvShared)) + 16 +
+           stages * static_cast<int>(sizeof(MkChunk));
 }
 
 int mk_max_stages(int x_bytes, int rec_chunks, int batch, int d_head) {

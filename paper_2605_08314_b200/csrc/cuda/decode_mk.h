@@ -17,6 +17,8 @@
 // SiLU.mul, logits, and writes the next phase's input planes.
 #pragma once
 
+#include <vector>
+
 #include "kernels.h"
 
 namespace fsvd::k {
@@ -123,6 +125,18 @@ struct alignas(16) MkPhase {
     MkVec v;
 };
 
+// One ring chunk of a CTA's weight stream, precomputed on the host (the
+// producer and the consumers never walk the work split on the device).
+struct alignas(16) MkChunk {
+    const char* src;   // weights, <= kChunkLines contiguous 2 KiB line tiles
+    uint16_t T;        // output tile
+    uint16_t kbase;    // input element offset of the chunk's first line
+    uint8_t nl;        // lines | 0x10: gate half (sub 1) | 0x20: last chunk of its output tile
+    uint8_t k;         // output tile index local to the CTA's range (chunk records)
+    uint8_t c;         // chunk index inside its run (record slot)
+    uint8_t ctile;     // chunk index inside its output tile
+};
+
 struct MkLaunch {
     const MkPhase* phases;  // device array
     int p_begin, p_end;
@@ -131,6 +145,12 @@ struct MkLaunch {
     int stages;             // ring depth (kChunkBytes each)
     int x_bytes;            // staged input region
     int rec_chunks;         // per-phase chunk records
+    int l2_ahead;           // weight chunks prefetched into L2 beyond the ring
+    const int* pos;         // length register (constant during a launch but for the final argmax phase)
+    const MkChunk* chunks;  // [cta][...] chunk records of every phase
+    const int* chunk_start; // [cta][nphases + 1] first record of each phase
+    int nphases;
+    volatile int* progress; // optional host-mapped [grid][16] for hang diagnosis
     unsigned long long* trace;  // optional [grid][phases][4] %globaltimer stamps
 };
 
@@ -147,6 +167,9 @@ int mk_out_tiles(const GemvSeg* seg, int nseg, int dual, int esize);
 void mk_split_stats(const GemvSeg* seg, int nseg, int dual, int esize, int grid, int* max_pieces, int* rec_ntl,
                     int* rec_c0, int* rec_c1);
 constexpr int kMkMaxLocalTiles = 64;
+// Chunk records of every GEMV phase for a grid of `grid` CTAs.
+void mk_build_chunks(const struct MkPhase* phases, int nphases, int grid, int esize, std::vector<MkChunk>& out,
+                     std::vector<int>& start);
 int mk_smem_bytes(int stages, int x_bytes, int rec_chunks, int batch, int d_head);
 int mk_max_stages(int x_bytes, int rec_chunks, int batch, int d_head);
 int mk_consumer_warps();

@@ -141,8 +141,17 @@ struct MkSplit {
         }
     }
     FSVD_HD int subs() const { return dual ? 2 : 1; }
+    // First unit of CTA c: the even split total*c/G snapped to the nearest
+    // output-tile boundary, so every tile has exactly one owner (no cross-CTA
+    // reduction). The imbalance this leaves is absorbed by HBM sharing: a CTA
+    // with one tile more pulls more bandwidth while the others idle.
     FSVD_HD int lo(int c, int G) const {
-        return static_cast<int>(static_cast<unsigned>(total) * static_cast<unsigned>(c) / static_cast<unsigned>(G));
+        if (c <= 0) return 0;
+        if (c >= G) return total;
+        const int U = static_cast<int>(static_cast<unsigned>(total) * static_cast<unsigned>(c) / static_cast<unsigned>(G));
+        int a, e;
+        tile_span(tile_of(U), a, e);
+        return U - a <= e - U ? a : e;
     }
     FSVD_HD int seg_of_tile(int T) const {
         int s = 0;

@@ -695,8 +695,41 @@ void Session::build_program() {
         throw ConfigError("decode megakernel: shared memory does not fit this (batch, shape): x " +
                           std::to_string(x_bytes_) + " B, " + std::to_string(rec_chunks_) + " chunk records");
     mk_smem_ = k::mk_smem_bytes(mk_stages_, x_bytes_, rec_chunks_, B_, dh);
+    // L2 prefetch distance (chunks per CTA beyond the ring): 16 x 16 KiB x 148 CTAs = 38 MB of the 126 MB L2
+    mk_l2_ahead_ = 0;
+    if (const char* e = std::getenv("FSVD_MK_L2_AHEAD")) mk_l2_ahead_ = std::max(0, std::atoi(e));
+    if (const char* e = std::getenv("FSVD_MK_PROGRESS"); e && e[0] == '1') {  // hang diagnosis (debug)
+        void* h = nullptr;
+        FSVD_CUDA(cudaHostAlloc(&h, 64ull * mk_grid_, cudaHostAllocMapped));
+        std::memset(h, 0xff, 64ull * mk_grid_);
+        mk_progress_host_ = static_cast<int*>(h);
+        void* d = nullptr;
+        FSVD_CUDA(cudaHostGetDevicePointer(&d, h, 0));
+        mk_progress_ = static_cast<volatile int*>(d);
+        std::thread([h = mk_progress_host_, n = mk_grid_] {
+            for (int it = 0; it < 600; ++it) {
+                std::this_thread::sleep_for(std::chrono::seconds(1));
+                if (const char* f = std::getenv("FSVD_MK_PROGRESS_DUMP"); f && it % 2 == 1) {
+                    FILE* o = std::fopen(f, "w");
+                    if (!o) continue;
+                    for (int c = 0; c < n; ++c) { std::fprintf(o, "%d", c); for (int q = 0; q < 16; ++q) std::fprintf(o, " %d", h[16 * c + q]); std::fprintf(o, "\n"); }
+                    std::fclose(o);
+                }
+            }
+        }).detach();
+    }
     if (const char* tr = std::getenv("FSVD_TRACE"); tr && tr[0] == '1')
         trace_ = static_cast<unsigned long long*>(dalloc(8ull * mk_grid_ * (ph_argmax_ + 1) * 16 + 8ull * 8192 * 4));
+    {  // precomputed chunk records of every CTA's weight stream
+        std::vector<k::MkChunk> ch;
+        std::vector<int> st;
+        k::mk_build_chunks(h_phases_.data(), static_cast<int>(h_phases_.size()), mk_grid_, m.esize, ch, st);
+        d_chunks_ = static_cast<k::MkChunk*>(dalloc(sizeof(k::MkChunk) * std::max<size_t>(1, ch.size())));
+        d_chunk_start_ = static_cast<int*>(dalloc(sizeof(int) * st.size()));
+        FSVD_CUDA(cudaMemcpyAsync(d_chunks_, ch.data(), sizeof(k::MkChunk) * ch.size(), cudaMemcpyHostToDevice, stream_));
+        FSVD_CUDA(cudaMemcpyAsync(d_chunk_start_, st.data(), sizeof(int) * st.size(), cudaMemcpyHostToDevice, stream_));
+        FSVD_CUDA(cudaStreamSynchronize(stream_));
+    }
     d_phases_ = static_cast<k::MkPhase*>(dalloc(sizeof(k::MkPhase) * h_phases_.size()));
     FSVD_CUDA(cudaMemcpyAsync(d_phases_, h_phases_.data(), sizeof(k::MkPhase) * h_phases_.size(),
                               cudaMemcpyHostToDevice, stream_));
@@ -713,6 +746,12 @@ void Session::mk_run(int p_begin, int p_end) {
     L.stages = mk_stages_;
     L.x_bytes = x_bytes_;
     L.rec_chunks = rec_chunks_;
+    L.l2_ahead = mk_l2_ahead_;
+    L.pos = pos_;
+    L.chunks = d_chunks_;
+    L.chunk_start = d_chunk_start_;
+    L.nphases = static_cast<int>(h_phases_.size());
+    L.progress = mk_progress_;
     if (trace_ && p_begin == 0 && p_end == ph_argmax_ + 1) L.trace = trace_;
     if (!k::mk_launch(m_->wt, B_, static_cast<int>(m_->cfg.d_head), L, stream_))
         throw CudaError("megakernel: no instantiation for this (dtype, batch, d_head)");

@@ -162,8 +162,12 @@ class Session {
     std::vector<k::MkPhase> h_phases_;
     int x_bytes_ = 0, rec_chunks_ = 0;
     k::MkPhase* d_phases_ = nullptr;
+    k::MkChunk* d_chunks_ = nullptr;
+    int* d_chunk_start_ = nullptr;
+    volatile int* mk_progress_ = nullptr;
+    int* mk_progress_host_ = nullptr;
     unsigned* mk_bar_ = nullptr;
-    int mk_smem_ = 0, mk_grid_ = 0, mk_splits_ = 0, mk_stages_ = 0;
+    int mk_smem_ = 0, mk_grid_ = 0, mk_splits_ = 0, mk_stages_ = 0, mk_l2_ahead_ = 16;
     int ph_head_ = 0, ph_argmax_ = 0, ph_pf_head_ = 0, ph_pf_argmax_ = 0;
     std::vector<int> ph_layer_begin_, ph_layer_end_;
     unsigned long long* trace_ = nullptr;  // FSVD_TRACE=1: per-phase globaltimer stamps of the full step
