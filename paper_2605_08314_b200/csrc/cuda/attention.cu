@@ -88,9 +88,207 @@ __global__ void __launch_bounds__(kPThreads) attn_prefill_kernel(const __grid_co
     for (int e = 0; e < slice; ++e) orow[part * slice + e] = from_f32<T>(acc[e] / l);
 }
 
+// ------------------------------------------------ tensor-core flash attention --
+// bf16 mode: 64 queries of one (sequence, head) per CTA, 4 warps x 16 rows;
+// 64-key tiles double-buffered in shared memory with cp.async; S = Q.K^T and
+// O += P.V on the tensor cores (mma.sync m16n8k16, fp32 accumulate), online
+// softmax in registers (the running-max recurrence of math.hpp:75-100).
+constexpr int kFQ = 64, kFK = 64, kFThreads = 128;
+
+__device__ __forceinline__ uint32_t smem_addr(const void* p) {
+    return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+__device__ __forceinline__ void cp_async16(void* dst, const void* src, bool pred) {
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(smem_addr(dst)), "l"(src), "r"(pred ? 16 : 0)
+                 : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory"); }
+__device__ __forceinline__ void ldsm_x4(uint32_t (&r)[4], const void* p) {
+    asm volatile("ldmatrix.sync.aligned.m8n8.x4.shared.b16 {%0,%1,%2,%3}, [%4];"
+                 : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3])
+                 : "r"(smem_addr(p)));
+}
+__device__ __forceinline__ void ldsm_x4_t(uint32_t (&r)[4], const void* p) {
+    asm volatile("ldmatrix.sync.aligned.m8n8.x4.trans.shared.b16 {%0,%1,%2,%3}, [%4];"
+                 : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3])
+                 : "r"(smem_addr(p)));
+}
+__device__ __forceinline__ void mma16816(float (&d)[4], const uint32_t (&a)[4], uint32_t b0, uint32_t b1) {
+    asm volatile(
+        "mma.sync.aligned.m16n8k16.row.col.f32.bf16.bf16.f32 {%0,%1,%2,%3}, {%4,%5,%6,%7}, {%8,%9}, {%0,%1,%2,%3};"
+        : "+f"(d[0]), "+f"(d[1]), "+f"(d[2]), "+f"(d[3])
+        : "r"(a[0]), "r"(a[1]), "r"(a[2]), "r"(a[3]), "r"(b0), "r"(b1));
+}
+__device__ __forceinline__ uint32_t pack_bf16x2(float lo, float hi) {
+    const __nv_bfloat162 v = __floats2bfloat162_rn(lo, hi);
+    return *reinterpret_cast<const uint32_t*>(&v);
+}
+
+template <int DH>
+__global__ void __launch_bounds__(kFThreads) attn_prefill_tc_kernel(const __grid_constant__ AttnPrefillArgs a) {
+    constexpr int LD = DH + 8;  // padded smem row (bf16): conflict-free ldmatrix
+    extern __shared__ __align__(128) __nv_bfloat16 fsm[];
+    __nv_bfloat16* Qs = fsm;                 // [kFQ][LD]
+    __nv_bfloat16* Ks = Qs + kFQ * LD;       // [2][kFK][LD]
+    __nv_bfloat16* Vs = Ks + 2 * kFK * LD;   // [2][kFK][LD]
+    const int qt = blockIdx.x, h = blockIdx.y, b = blockIdx.z;
+    const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31, g = lane >> 2, t4 = lane & 3;
+    const int q0 = qt * kFQ;
+    const __nv_bfloat16* Q = static_cast<const __nv_bfloat16*>(a.q) + static_cast<long long>(b) * a.T * a.q_ld + h * DH;
+    const __nv_bfloat16* K = static_cast<const __nv_bfloat16*>(a.kcache) + b * a.cache_bstride + h * a.cache_hstride;
+    const __nv_bfloat16* V = static_cast<const __nv_bfloat16*>(a.vcache) + b * a.cache_bstride + h * a.cache_hstride;
+    const int last_q = min(a.T, q0 + kFQ) - 1;
+    const int kend = a.p0 + last_q + 1;
+    const int ntiles = (kend + kFK - 1) / kFK;
+    constexpr int CPR = DH / 8;  // 16-byte chunks per row
+
+    // Q tile + first K/V tile
+    for (int i = tid; i < kFQ * CPR; i += kFThreads) {
+        const int r = i / CPR, c = (i % CPR) * 8;
+        const bool ok = q0 + r < a.T;
+        cp_async16(Qs + r * LD + c, Q + static_cast<long long>(ok ? q0 + r : 0) * a.q_ld + c, ok);
+    }
+    auto load_kv = [&](int tile, int buf) {
+        const int k0 = tile * kFK;
+        for (int i = tid; i < kFK * CPR; i += kFThreads) {
+            const int r = i / CPR, c = (i % CPR) * 8;
+            const bool ok = k0 + r < kend;
+            const long long off = static_cast<long long>(ok ? k0 + r : 0) * DH + c;
+            cp_async16(Ks + (buf * kFK + r) * LD + c, K + off, ok);
+            cp_async16(Vs + (buf * kFK + r) * LD + c, V + off, ok);
+        }
+    };
+    load_kv(0, 0);
+    cp_async_commit();
+
+    // this thread's two query rows: g and g + 8 of the warp's 16
+    const int rq0 = warp * 16 + g, rq1 = rq0 + 8;
+    const int pos0 = a.p0 + min(q0 + rq0, a.T - 1), pos1 = a.p0 + min(q0 + rq1, a.T - 1);
+    const float sl2 = a.scale * 1.4426950408889634f;  // scores in log2 units
+    float m0 = -CUDART_INF_F, m1 = -CUDART_INF_F, l0 = 0.f, l1 = 0.f;
+    float o[DH / 8][4];
+#pragma unroll
+    for (int n = 0; n < DH / 8; ++n) o[n][0] = o[n][1] = o[n][2] = o[n][3] = 0.f;
+    uint32_t qf[DH / 16][4];
+
+    for (int tile = 0; tile < ntiles; ++tile) {
+        const int buf = tile & 1;
+        if (tile + 1 < ntiles) load_kv(tile + 1, buf ^ 1);
+        cp_async_commit();
+        cp_async_wait<1>();
+        __syncthreads();
+        if (tile == 0) {
+#pragma unroll
+            for (int kk = 0; kk < DH / 16; ++kk)
+                ldsm_x4(qf[kk], Qs + (warp * 16 + (lane & 7) + 8 * ((lane >> 3) & 1)) * LD + kk * 16 + 8 * (lane >> 4));
+        }
+        const __nv_bfloat16* Kb = Ks + buf * kFK * LD;
+        const __nv_bfloat16* Vb = Vs + buf * kFK * LD;
+        // S = Q K^T : 16 x 64 per warp (8 key n-tiles)
+        float sc[kFK / 8][4];
+#pragma unroll
+        for (int n = 0; n < kFK / 8; ++n) sc[n][0] = sc[n][1] = sc[n][2] = sc[n][3] = 0.f;
+#pragma unroll
+        for (int kk = 0; kk < DH / 16; ++kk)
+#pragma unroll
+            for (int np = 0; np < kFK / 16; ++np) {
+                uint32_t kb[4];
+                ldsm_x4(kb, Kb + (np * 16 + (lane & 7) + 8 * (lane >> 4)) * LD + kk * 16 + 8 * ((lane >> 3) & 1));
+                mma16816(sc[2 * np], qf[kk], kb[0], kb[1]);
+                mma16816(sc[2 * np + 1], qf[kk], kb[2], kb[3]);
+            }
+        // causal mask + online softmax (per row: max over the quad)
+        const int k0 = tile * kFK;
+        float mx0 = -CUDART_INF_F, mx1 = -CUDART_INF_F;
+#pragma unroll
+        for (int n = 0; n < kFK / 8; ++n) {
+            const int j = k0 + n * 8 + 2 * t4;
+            sc[n][0] = j <= pos0 ? sc[n][0] * sl2 : -CUDART_INF_F;
+            sc[n][1] = j + 1 <= pos0 ? sc[n][1] * sl2 : -CUDART_INF_F;
+            sc[n][2] = j <= pos1 ? sc[n][2] * sl2 : -CUDART_INF_F;
+            sc[n][3] = j + 1 <= pos1 ? sc[n][3] * sl2 : -CUDART_INF_F;
+            mx0 = fmaxf(mx0, fmaxf(sc[n][0], sc[n][1]));
+            mx1 = fmaxf(mx1, fmaxf(sc[n][2], sc[n][3]));
+        }
+        mx0 = fmaxf(mx0, __shfl_xor_sync(0xffffffffu, mx0, 1));
+        mx0 = fmaxf(mx0, __shfl_xor_sync(0xffffffffu, mx0, 2));
+        mx1 = fmaxf(mx1, __shfl_xor_sync(0xffffffffu, mx1, 1));
+        mx1 = fmaxf(mx1, __shfl_xor_sync(0xffffffffu, mx1, 2));
+        const float mn0 = fmaxf(m0, mx0), mn1 = fmaxf(m1, mx1);
+        const float r0 = mn0 == -CUDART_INF_F ? 1.f : exp2f(m0 - mn0);
+        const float r1 = mn1 == -CUDART_INF_F ? 1.f : exp2f(m1 - mn1);
+        m0 = mn0;
+        m1 = mn1;
+        float s0 = 0.f, s1 = 0.f;
+        uint32_t pf[kFK / 16][4];
+#pragma unroll
+        for (int n = 0; n < kFK / 8; ++n) {
+            const float p0v = mn0 == -CUDART_INF_F ? 0.f : exp2f(sc[n][0] - mn0);
+            const float p1v = mn0 == -CUDART_INF_F ? 0.f : exp2f(sc[n][1] - mn0);
+            const float p2v = mn1 == -CUDART_INF_F ? 0.f : exp2f(sc[n][2] - mn1);
+            const float p3v = mn1 == -CUDART_INF_F ? 0.f : exp2f(sc[n][3] - mn1);
+            s0 += p0v + p1v;
+            s1 += p2v + p3v;
+            // P as the A operand of P.V: n-tile 2kk -> a0/a1, 2kk+1 -> a2/a3
+            pf[n >> 1][(n & 1) * 2 + 0] = pack_bf16x2(p0v, p1v);
+            pf[n >> 1][(n & 1) * 2 + 1] = pack_bf16x2(p2v, p3v);
+        }
+        l0 = l0 * r0 + s0;
+        l1 = l1 * r1 + s1;
+#pragma unroll
+        for (int n = 0; n < DH / 8; ++n) {
+            o[n][0] *= r0;
+            o[n][1] *= r0;
+            o[n][2] *= r1;
+            o[n][3] *= r1;
+        }
+        // O += P V : k = 64 keys (4 steps), n = DH
+#pragma unroll
+        for (int kk = 0; kk < kFK / 16; ++kk)
+#pragma unroll
+            for (int dp = 0; dp < DH / 16; ++dp) {
+                uint32_t vb[4];
+                ldsm_x4_t(vb, Vb + (kk * 16 + (lane & 7) + 8 * ((lane >> 3) & 1)) * LD + dp * 16 + 8 * (lane >> 4));
+                mma16816(o[2 * dp], pf[kk], vb[0], vb[1]);
+                mma16816(o[2 * dp + 1], pf[kk], vb[2], vb[3]);
+            }
+        __syncthreads();
+    }
+    // row sums over the quad, normalize, store
+    l0 += __shfl_xor_sync(0xffffffffu, l0, 1);
+    l0 += __shfl_xor_sync(0xffffffffu, l0, 2);
+    l1 += __shfl_xor_sync(0xffffffffu, l1, 1);
+    l1 += __shfl_xor_sync(0xffffffffu, l1, 2);
+    const float i0 = 1.f / l0, i1 = 1.f / l1;
+    __nv_bfloat16* O = static_cast<__nv_bfloat16*>(a.out) + static_cast<long long>(b) * a.T * a.out_ld + h * DH;
+    const int t0 = q0 + rq0, t1 = q0 + rq1;
+#pragma unroll
+    for (int n = 0; n < DH / 8; ++n) {
+        const int c = n * 8 + 2 * t4;
+        if (t0 < a.T)
+            *reinterpret_cast<uint32_t*>(O + static_cast<long long>(t0) * a.out_ld + c) = pack_bf16x2(o[n][0] * i0, o[n][1] * i0);
+        if (t1 < a.T)
+            *reinterpret_cast<uint32_t*>(O + static_cast<long long>(t1) * a.out_ld + c) = pack_bf16x2(o[n][2] * i1, o[n][3] * i1);
+    }
+}
+
 }  // namespace
 
 void attn_prefill(WType wt, const AttnPrefillArgs& a, cudaStream_t s) {
+    if (wt == kBF16 && (a.d_head == 64 || a.d_head == 128) && a.q_ld % 8 == 0 && a.out_ld % 8 == 0) {
+        dim3 grid((a.T + kFQ - 1) / kFQ, a.n_heads, a.batch);
+        const int smem = (kFQ + 4 * kFK) * (a.d_head + 8) * 2;
+        if (a.d_head == 128) {
+            cudaFuncSetAttribute(attn_prefill_tc_kernel<128>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+            attn_prefill_tc_kernel<128><<<grid, kFThreads, smem, s>>>(a);
+        } else {
+            cudaFuncSetAttribute(attn_prefill_tc_kernel<64>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+            attn_prefill_tc_kernel<64><<<grid, kFThreads, smem, s>>>(a);
+        }
+        return;
+    }
     dim3 grid((a.T + kPQ - 1) / kPQ, a.n_heads, a.batch);
     const int smem = (kPK * (a.d_head + 1) + kPK * a.d_head) * static_cast<int>(sizeof(float));
 #define FSVD_PRE(DH)                                                                                   \
