@@ -49,3 +49,14 @@ def test_errors_cross_the_boundary_as_status(fsvd):
     with pytest.raises(fsvd.InvalidArgument):
         fsvd._check(L.fsvd_session_reset(None))
     assert fsvd.lib().fsvd_version()
+
+
+def test_cpp_wrapper_rethrows_reference_exceptions(fsvd, tmp_path):
+    """include/fsvd/runtime.hpp: C++ callers keep catch (fsvd::FormatError&)."""
+    exe = tmp_path / "wrapper_check"
+    cmd = ["g++", "-std=c++20", "-O1", "-I", str(ROOT / "include"), str(ROOT / "tests/cpp/wrapper_check.cpp"),
+           "-o", str(exe), "-L", str(fsvd.LIB_PATH.parent), "-lfsvd_b200",
+           f"-Wl,-rpath,{fsvd.LIB_PATH.parent}"]
+    subprocess.run(cmd, check=True, capture_output=True, text=True)
+    r = subprocess.run([str(exe)], capture_output=True, text=True)
+    assert r.returncode == 0 and "OK" in r.stdout, r.stdout + r.stderr
