@@ -19,6 +19,7 @@
 // applies silu(gate) * up in the epilogue, so up/gate never reach memory.
 #include <cuda.h>
 
+#include <algorithm>
 #include <stdexcept>
 #include <string>
 
@@ -46,6 +47,7 @@ struct TcArgs {
     CUtensorMap xmap;  // X [rows][x_ld] bf16, box 64 x 128, SWIZZLE_128B
     GemmArgs g;
     int seg_tiles[3];  // BN-wide output tiles per segment
+    int splits;        // split-K factor (blockIdx.z = split; > 1 only for kGemmStore)
 };
 
 // ----------------------------------------------------------------- PTX ----
@@ -206,12 +208,14 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_tc_kernel(const __grid_const
                 const GemvSeg& sj = seg_of(j);
                 const WLayout lay = sj.layout(2);
                 const int nk = lay.nlines();
+                const int kb0 = nk * static_cast<int>(blockIdx.z) / A.splits;
+                const int kb1 = nk * (static_cast<int>(blockIdx.z) + 1) / A.splits;
                 const int t0 = n0 / 16;
                 const int nt = min(BN / 16, lay.ntiles() - t0);
                 const uint32_t bytes = kABytes + static_cast<uint32_t>(nt) * kLineTileBytes;
                 const char* wbase = static_cast<const char*>(sj.w) + static_cast<size_t>(t0) * lay.tile_bytes();
 #pragma unroll 1
-                for (int kb = 0; kb < nk; ++kb, ++it) {
+                for (int kb = kb0; kb < kb1; ++kb, ++it) {
                     const int st = it % C::kStages;
                     const uint32_t ph = (it / C::kStages) & 1;
                     mbar_wait(&empty[st], ph ^ 1);
@@ -233,9 +237,11 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_tc_kernel(const __grid_const
 #pragma unroll 1
             for (int j = 0; j < kAcc; ++j) {
                 const int nk = seg_of(j).layout(2).nlines();
+                const int kb0 = nk * static_cast<int>(blockIdx.z) / A.splits;
+                const int kb1 = nk * (static_cast<int>(blockIdx.z) + 1) / A.splits;
                 const uint32_t tacc = tmem_base + static_cast<uint32_t>(j * BN);
 #pragma unroll 1
-                for (int kb = 0; kb < nk; ++kb, ++it) {
+                for (int kb = kb0; kb < kb1; ++kb, ++it) {
                     const int st = it % C::kStages;
                     const uint32_t ph = (it / C::kStages) & 1;
                     mbar_wait(&full[st], ph);
@@ -245,7 +251,7 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_tc_kernel(const __grid_const
                     const uint64_t da = sw128_desc(sa), db = sw128_desc(sb);
 #pragma unroll
                     for (int k = 0; k < BK / 16; ++k)  // +32 B per K=16 step inside the 128 B swizzle atom
-                        tc_mma(tacc, da + 2 * k, db + 2 * k, idesc, (kb | k) != 0 ? 1u : 0u);
+                        tc_mma(tacc, da + 2 * k, db + 2 * k, idesc, (kb != kb0 || k != 0) ? 1u : 0u);
                     tc_commit(&empty[st]);
                 }
             }
@@ -272,6 +278,11 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_tc_kernel(const __grid_const
                 for (int i = 0; i < 32; ++i) v[i] = silu_mul(gt[i], v[i]);
                 store_bf16x32(static_cast<__nv_bfloat16*>(g.y) + static_cast<long long>(t) * g.y_ld + sg.y_off + n, v,
                               valid);
+            } else if (g.epi == kGemmStore && A.splits > 1) {  // fp32 partial of this K split
+                float* w = g.ws + (static_cast<size_t>(blockIdx.z) * g.M + t) * g.y_ld + sg.y_off + n;
+#pragma unroll
+                for (int i = 0; i < 32; ++i)
+                    if (i < valid) w[i] = v[i];
             } else if (g.epi == kGemmStore) {
                 store_bf16x32(static_cast<__nv_bfloat16*>(g.y) + static_cast<long long>(t) * g.y_ld + sg.y_off + n, v,
                               valid);
@@ -331,6 +342,21 @@ EncodeTiled encode_fn() {
     return fn;
 }
 
+// Split-K reduction: Y[t][y_off + n] = bf16(sum_z ws[z][t][y_off + n]) in split order.
+__global__ void splitk_reduce_kernel(const __grid_constant__ TcArgs A) {
+    const GemmArgs& g = A.g;
+    const int t = blockIdx.y;
+    for (int s = 0; s < g.nseg; ++s) {
+        const GemvSeg& sg = g.seg[s];
+        for (int n = blockIdx.x * blockDim.x + threadIdx.x; n < sg.rows; n += gridDim.x * blockDim.x) {
+            const size_t c = static_cast<size_t>(t) * g.y_ld + sg.y_off + n;
+            float acc = g.ws[c];
+            for (int z = 1; z < A.splits; ++z) acc += g.ws[static_cast<size_t>(z) * g.M * g.y_ld + c];
+            static_cast<__nv_bfloat16*>(g.y)[c] = __float2bfloat16_rn(acc);
+        }
+    }
+}
+
 template <int BN, bool DUAL>
 void launch(const TcArgs& ta, int tiles, int M, cudaStream_t s) {
     using C = Cfg<BN>;
@@ -339,8 +365,9 @@ void launch(const TcArgs& ta, int tiles, int M, cudaStream_t s) {
         cudaFuncSetAttribute(gemm_tc_kernel<BN, DUAL>, cudaFuncAttributeMaxDynamicSharedMemorySize, C::kSmem);
         attr = true;
     }
-    dim3 grid((M + BM - 1) / BM, tiles);
+    dim3 grid((M + BM - 1) / BM, tiles, ta.splits);
     gemm_tc_kernel<BN, DUAL><<<grid, kThreads, C::kSmem, s>>>(ta);
+    if (ta.splits > 1) splitk_reduce_kernel<<<dim3(8, M), 256, 0, s>>>(ta);
 }
 
 }  // namespace
@@ -371,6 +398,17 @@ void gemm_tc(const GemmArgs& a, int x_rows, cudaStream_t s) {
     for (int i = 0; i < nseg; ++i) {
         ta.seg_tiles[i] = (a.seg[i].rows + BN - 1) / BN;
         tiles += ta.seg_tiles[i];
+    }
+    // split K when the output tiles cannot fill the SMs (skinny rank-space
+    // projections at small token counts); deterministic fixed-order reduction
+    ta.splits = 1;
+    const int mt = (a.M + BM - 1) / BM;
+    if (!dual && a.epi == kGemmStore && a.ws) {
+        int nk_min = 1 << 30;
+        for (int i = 0; i < a.nseg; ++i) nk_min = std::min(nk_min, a.seg[i].layout(2).nlines());
+        int sp = 148 / std::max(1, tiles * mt);
+        sp = std::min({sp, 4, nk_min / 4});
+        if (sp > 1 && static_cast<size_t>(sp) * a.M * a.y_ld <= a.ws_floats) ta.splits = sp;
     }
     if (dual)
         launch<BN, true>(ta, tiles, a.M, s);

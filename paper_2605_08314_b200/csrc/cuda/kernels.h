@@ -75,6 +75,10 @@ struct GemmArgs {
     void* kcache;
     void* vcache;
     long long cache_bstride, cache_hstride;
+    // split-K scratch for the plain-store epilogue (few output tiles): fp32
+    // [splits][M][y_ld]; null disables split-K
+    float* ws;
+    size_t ws_floats;
 };
 void gemm(WType wt, const GemmArgs& a, cudaStream_t s);       // dispatch: tcgen05 (bf16) / CUDA cores (f32)
 void gemm_simt(WType wt, const GemmArgs& a, cudaStream_t s);  // CUDA-core path

@@ -856,8 +856,11 @@ void Session::ensure_prefill_workspace(size_t rows) {
     pf_h_ = dalloc(rows * m.ldff * es);
     pf_pd_ = dalloc(rows * ld_d_ * es);
     pf_tok_ = static_cast<int32_t*>(dalloc(rows * 4));
+    // split-K scratch (only used while rows <= 1024: few output tiles)
+    pf_ws_floats_ = 4ull * std::min<size_t>(rows, 1024) * std::max({ld_qkv_, ld_o_, ld_ug_, ld_d_});
+    pf_ws_ = m.wt == k::kBF16 ? static_cast<float*>(dalloc(4 * pf_ws_floats_)) : nullptr;
     pf_rows_ = rows;
-    stats_.allocs += 10;
+    stats_.allocs += 11;
 }
 
 // One prefill chunk: tokens [b][t0 .. t0+Tc) of a [B][T_total] prompt.
@@ -893,6 +896,10 @@ void Session::prefill_chunk(const int32_t* d_tokens, size_t T_total, size_t t0, 
         g.vcache = vc;
         g.cache_bstride = cache_bstride_;
         g.cache_hstride = cache_hstride_;
+        if (M <= 1024) {
+            g.ws = pf_ws_;
+            g.ws_floats = pf_ws_floats_;
+        }
         k::gemm(m.wt, g, stream_);
     };
     for (size_t l = 0; l < c.n_layers; ++l) {

@@ -185,6 +185,8 @@ class Session {
     void *pf_xn_ = nullptr, *pf_pqkv_ = nullptr, *pf_q_ = nullptr, *pf_att_ = nullptr, *pf_po_ = nullptr,
          *pf_pug_ = nullptr, *pf_h_ = nullptr, *pf_pd_ = nullptr;
     int32_t* pf_tok_ = nullptr;
+    float* pf_ws_ = nullptr;
+    size_t pf_ws_floats_ = 0;
 };
 
 }  // namespace fsvd::rt
