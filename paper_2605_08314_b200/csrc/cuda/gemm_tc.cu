@@ -392,9 +392,18 @@ void gemm_tc(const GemmArgs& a, int x_rows, cudaStream_t s) {
                                    CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
     if (r != CUDA_SUCCESS) throw std::runtime_error("cuTensorMapEncodeTiled failed: " + std::to_string(int(r)));
     const bool dual = a.epi == kGemmSilu;
-    constexpr int BN = 128;
-    int tiles = 0;
     const int nseg = dual ? 1 : a.nseg;
+    const int mt = (a.M + BM - 1) / BM;
+    auto count_tiles = [&](int bn) {
+        int t = 0;
+        for (int i = 0; i < nseg; ++i) t += (a.seg[i].rows + bn - 1) / bn;
+        return t;
+    };
+    // 128 x 256 tiles (A tile reused over twice the outputs, half the CTAs) when
+    // they still cover the SMs; 128 x 128 otherwise
+    const bool wide = count_tiles(256) * mt >= 120;
+    const int BN = wide ? 256 : 128;
+    int tiles = 0;
     for (int i = 0; i < nseg; ++i) {
         ta.seg_tiles[i] = (a.seg[i].rows + BN - 1) / BN;
         tiles += ta.seg_tiles[i];
@@ -402,7 +411,6 @@ void gemm_tc(const GemmArgs& a, int x_rows, cudaStream_t s) {
     // split K when the output tiles cannot fill the SMs (skinny rank-space
     // projections at small token counts); deterministic fixed-order reduction
     ta.splits = 1;
-    const int mt = (a.M + BM - 1) / BM;
     if (!dual && a.epi == kGemmStore && a.ws) {
         int nk_min = 1 << 30;
         for (int i = 0; i < a.nseg; ++i) nk_min = std::min(nk_min, a.seg[i].layout(2).nlines());
@@ -410,10 +418,17 @@ void gemm_tc(const GemmArgs& a, int x_rows, cudaStream_t s) {
         sp = std::min({sp, 4, nk_min / 4});
         if (sp > 1 && static_cast<size_t>(sp) * a.M * a.y_ld <= a.ws_floats) ta.splits = sp;
     }
-    if (dual)
-        launch<BN, true>(ta, tiles, a.M, s);
-    else
-        launch<BN, false>(ta, tiles, a.M, s);
+    if (wide) {
+        if (dual)
+            launch<256, true>(ta, tiles, a.M, s);
+        else
+            launch<256, false>(ta, tiles, a.M, s);
+    } else {
+        if (dual)
+            launch<128, true>(ta, tiles, a.M, s);
+        else
+            launch<128, false>(ta, tiles, a.M, s);
+    }
 }
 
 }  // namespace fsvd::k
