@@ -400,6 +400,37 @@ __device__ __forceinline__ void load_kv_row(const T* p, float* out) {
     }
 }
 
+// K/V row slice of one lane kept packed while in flight (bf16: 4 values in a uint2)
+template <typename E, int PER>
+struct KvRaw {
+    struct T4 {
+        float v[PER];
+    };
+    using T = T4;
+    static __device__ __forceinline__ T4 load(const E* p) {
+        T4 r;
+        load_kv_row<E, PER>(p, r.v);
+        return r;
+    }
+    static __device__ __forceinline__ void unpack(const T4& r, float* out) {
+#pragma unroll
+        for (int e = 0; e < PER; ++e) out[e] = r.v[e];
+    }
+};
+template <>
+struct KvRaw<__nv_bfloat16, 4> {
+    using T = uint2;
+    static __device__ __forceinline__ uint2 load(const __nv_bfloat16* p) {
+        return __ldcg(reinterpret_cast<const uint2*>(p));
+    }
+    static __device__ __forceinline__ void unpack(const uint2& v, float* out) {
+        out[0] = bf16lo(v.x);
+        out[1] = bf16hi(v.x);
+        out[2] = bf16lo(v.y);
+        out[3] = bf16hi(v.y);
+    }
+};
+
 template <typename W, int B, int DH>
 __device__ void attn_phase(const MkAttn& a, const Smem& sm, int tid, int cta, int G, int pos) {
     constexpr int PER = DH / 32, KU = 8, ST = DH + 2;
@@ -408,7 +439,11 @@ __device__ void attn_phase(const MkAttn& a, const Smem& sm, int tid, int cta, in
     RowSplit rs{B * a.n_heads * len};
     const int r0 = rs.lo(cta, G), r1 = rs.lo(cta + 1, G);
     float* wst = sm.rec;  // [warps][DH + 2]: acc, l, m
-    for (int bh = r0 / len; bh * len < r1; ++bh) {
+    // heads in reverse: a CTA publishes its share of the head it shares with
+    // the next CTA first, then finalizes the heads whose newest keys it holds
+    // (their other contributors published first too) -- no wait chains
+    const int bh_first = r0 / len, bh_last = r1 > r0 ? (r1 - 1) / len : bh_first - 1;
+    for (int bh = bh_last; bh >= bh_first; --bh) {
         const int lo_bh = bh * len, hi_bh = lo_bh + len;
         const int j0 = static_cast<int>((r0 > lo_bh ? r0 : lo_bh) - lo_bh);
         const int j1 = static_cast<int>((r1 < hi_bh ? r1 : hi_bh) - lo_bh);
@@ -428,14 +463,26 @@ __device__ void attn_phase(const MkAttn& a, const Smem& sm, int tid, int cta, in
         float m = -CUDART_INF_F, l = 0.f, acc[PER];
 #pragma unroll
         for (int e = 0; e < PER; ++e) acc[e] = 0.f;
+        // software pipeline: the next batch of KU keys is in flight while this one is reduced
+        using Raw = typename KvRaw<W, PER>::T;
+        Raw kraw[KU], vraw[KU];
+        auto load_batch = [&](int kb, Raw (&kq)[KU], Raw (&vq)[KU]) {
+#pragma unroll
+            for (int u = 0; u < KU; ++u) {
+                const int jj = min(kb + u, k1 - 1);  // clamp: duplicate loads are masked below
+                kq[u] = KvRaw<W, PER>::load(Kc + static_cast<long long>(jj) * DH + lane * PER);
+                vq[u] = KvRaw<W, PER>::load(Vc + static_cast<long long>(jj) * DH + lane * PER);
+            }
+        };
+        if (k0 < k1) load_batch(k0, kraw, vraw);
         for (int kb = k0; kb < k1; kb += KU) {
             float kr[KU][PER], vr[KU][PER];
 #pragma unroll
             for (int u = 0; u < KU; ++u) {
-                const int jj = min(kb + u, k1 - 1);  // clamp: duplicate loads are masked below
-                load_kv_row<W, PER>(Kc + static_cast<long long>(jj) * DH + lane * PER, kr[u]);
-                load_kv_row<W, PER>(Vc + static_cast<long long>(jj) * DH + lane * PER, vr[u]);
+                KvRaw<W, PER>::unpack(kraw[u], kr[u]);
+                KvRaw<W, PER>::unpack(vraw[u], vr[u]);
             }
+            if (kb + KU < k1) load_batch(kb + KU, kraw, vraw);
             float sc[KU];
             float mb = -CUDART_INF_F;
 #pragma unroll
@@ -475,30 +522,42 @@ __device__ void attn_phase(const MkAttn& a, const Smem& sm, int tid, int cta, in
         for (int w = 0; w < kConsumerWarps; ++w) M = fmaxf(M, wst[w * ST + DH + 1]);
         float* part = a.partial + static_cast<long long>(bh) * a.splits * ST;
         if (np > 1) {
+            // Shared head: the CTA holding the newest keys (slot np-1) finalizes;
+            // the others publish their partial with a release increment (no wait).
             const int slot = rs.nonempty(c0, cta, G);
+            const bool fin = slot == np - 1;
+            float* own = fin ? sm.misc + 96 : part + slot * ST;  // (misc[96..226) is free here)
             for (int e = tid; e < DH + 1; e += kConsumerThreads) {
                 float t = 0.f;
                 for (int w = 0; w < kConsumerWarps; ++w) {
                     const float mw = wst[w * ST + DH + 1];
                     if (mw != -CUDART_INF_F) t += wst[w * ST + e] * expf(mw - M);
                 }
-                part[slot * ST + e] = t;
+                own[e] = t;
             }
-            if (tid == 0) part[slot * ST + DH + 1] = M;
-            fence_acq_rel_gpu();
+            if (tid == 0) own[DH + 1] = M;
             consumer_sync();
-            if (tid == 0) sm.misc[64] = atom_add_acq_rel(a.count + bh, 1u) == static_cast<unsigned>(np - 1) ? 1.f : 0.f;
-            consumer_sync();
-            if (sm.misc[64] != 0.f) {
-                fence_acq_rel_gpu();
+            if (!fin) {
+                if (tid == 0) {
+                    fence_acq_rel_gpu();
+                    red_release_add(a.count + bh, 1u);
+                }
+            } else {
+                if (tid == 0)
+                    while (ld_acquire(a.count + bh) < static_cast<unsigned>(np - 1)) {
+                    }
+                consumer_sync();
+                auto pm = [&](int q) { return q < np - 1 ? __ldcg(part + q * ST + DH + 1) : own[DH + 1]; };
+                auto pl = [&](int q) { return q < np - 1 ? __ldcg(part + q * ST + DH) : own[DH]; };
                 float MM = -CUDART_INF_F;
-                for (int q = 0; q < np; ++q) MM = fmaxf(MM, __ldcg(part + q * ST + DH + 1));
+                for (int q = 0; q < np; ++q) MM = fmaxf(MM, pm(q));
                 float L = 0.f;
-                for (int q = 0; q < np; ++q) L += __ldcg(part + q * ST + DH) * expf(__ldcg(part + q * ST + DH + 1) - MM);
+                for (int q = 0; q < np; ++q) L += pl(q) * expf(pm(q) - MM);
                 const float invL = 1.0f / L;
                 for (int e = tid; e < DH; e += kConsumerThreads) {
                     float o = 0.f;
-                    for (int q = 0; q < np; ++q) o = fmaf(__ldcg(part + q * ST + e), expf(__ldcg(part + q * ST + DH + 1) - MM), o);
+                    for (int q = 0; q < np; ++q)
+                        o = fmaf(q < np - 1 ? __ldcg(part + q * ST + e) : own[e], expf(pm(q) - MM), o);
                     PlaneIO<W>::put(a.out, b, h * DH + e, o * invL);
                 }
                 if (tid == 0) a.count[bh] = 0u;
