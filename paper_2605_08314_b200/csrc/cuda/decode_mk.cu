@@ -370,7 +370,7 @@ __device__ void gemv_phase(const MkGemv& g, const Smem& sm, GemvShared& sh, int 
                 }
                 v[sb][b] = acc;
             }
-        if (!exchange_pieces<B>(g, sp, T, cta, G, lane, v)) continue;
+        // (tile-aligned CTA ranges: every tile has exactly one owner, no exchange)
         finalize_rows<W, B>(g, sh, T, lane, v, inv);
     }
     if (prog && lane == 0) prog[2 + warp] = 3000000 + nchunks;

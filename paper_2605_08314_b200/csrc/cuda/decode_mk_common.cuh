@@ -349,22 +349,33 @@ struct ChunkDot;
 
 template <int B>
 struct ChunkDot<__nv_bfloat16, B> {
+    // A fragments by ldmatrix.x4 straight from the swizzled line tile (each
+    // 8x8 matrix = 8 rows x 16 B at distinct XOR-swizzled chunks: conflict-free),
+    // B fragments = 4-byte pairs of the staged x planes.
     static __device__ __forceinline__ void run(const char* buf, int nl, const __nv_bfloat16* x, int x_len, int kbase,
                                                int lane, float* rec) {
         const int g = lane >> 2, t = lane & 3;
-        const __nv_bfloat16* xp = x + g * x_len + kbase + 4 * t;
+        const int r = (lane & 7) + 8 * ((lane >> 3) & 1);  // row this lane addresses for ldmatrix
+        const int hi = lane >> 4;                          // which 16-B chunk of the k-step
+        const __nv_bfloat16* xp = x + g * x_len + kbase + 2 * t;
+        const uint32_t a_row = static_cast<uint32_t>(__cvta_generic_to_shared(buf)) + r * kLineBytes;
         float d[4][4] = {};
 #pragma unroll 2
         for (int l = 0; l < nl; ++l) {
-            const char* lb = buf + l * kLineTileBytes;
+            const uint32_t lrow = a_row + l * kLineTileBytes;
 #pragma unroll
             for (int j = 0; j < 4; ++j) {
-                const int off = ((((2 * j + (t >> 1)) ^ g) & 7) << 4) | ((t & 1) << 3);
-                const uint2 r0 = *reinterpret_cast<const uint2*>(lb + g * kLineBytes + off);
-                const uint2 r1 = *reinterpret_cast<const uint2*>(lb + (g + 8) * kLineBytes + off);
-                uint2 xv = make_uint2(0u, 0u);
-                if (g < 2 * B) xv = *reinterpret_cast<const uint2*>(xp + l * 64 + 16 * j);
-                mma_bf16(d[j], r0.x, r1.x, r0.y, r1.y, xv.x, xv.y);
+                uint32_t a0, a1, a2, a3;
+                const uint32_t addr = lrow + ((((2 * j + hi) ^ r) & 7) << 4);
+                asm volatile("ldmatrix.sync.aligned.m8n8.x4.shared.b16 {%0,%1,%2,%3}, [%4];"
+                             : "=r"(a0), "=r"(a1), "=r"(a2), "=r"(a3)
+                             : "r"(addr));
+                uint32_t b0 = 0u, b1 = 0u;
+                if (g < 2 * B) {
+                    b0 = *reinterpret_cast<const uint32_t*>(xp + l * 64 + 16 * j);
+                    b1 = *reinterpret_cast<const uint32_t*>(xp + l * 64 + 16 * j + 8);
+                }
+                mma_bf16(d[j], a0, a1, a2, a3, b0, b1);
             }
         }
         if (t < B) {

@@ -79,13 +79,40 @@ def main():
     f_load = med(tr[:, :, 11] - tr[:, :, 10])
     f_rows = med(tr[:, :, 12] - np.maximum(tr[:, :, 11], tr[:, :, 8]))
     f_tail = med(tr[:, :, 4] - tr[:, :, 12])
+    dur = (tr[:, :, 4] - tr[:, :, 0]) / 1e3
+    print("per-CTA phase duration (us): median p90 max | span | start skew (max-min start)")
+    for i, n in enumerate(names):
+        if n.startswith(f"L{mid}.") or n == "head":
+            st = tr[:, i, 0]
+            print(f"{n:10s} {np.median(dur[:, i]):6.2f} {np.percentile(dur[:, i], 90):6.2f} {dur[:, i].max():6.2f} | "
+                  f"{(end[i] - start[i]) / 1e3:6.2f} | {(st.max() - st.min()) / 1e3:6.2f}")
     print("finalize breakdown (warp 0, first tile): recsum  fence  atomic  pieceld  rows  tail(other warps+sync)")
     for i, n in enumerate(names):
         if n.startswith(f"L{mid}.") or n == "head":
             print(f"{n:10s} {f_sum[i]:6.2f} {f_fence[i]:6.2f} {f_atom[i]:6.2f} {f_load[i]:6.2f} {f_rows[i]:6.2f} {f_tail[i]:6.2f}")
     spans = end - start
+    cta0_timeline(s, tr, names, mid)
     print(f"sum: stage {stage.sum():.1f} us, chunks {chunks.sum():.1f} us, finalize {fin.sum():.1f} us, "
           f"phase spans {spans.sum() / 1e3:.1f} us")
+
+
+
+def cta0_timeline(s, tr, names, mid):
+    """CTA 0: per phase of the middle layer, its chunks' ready / done times
+    relative to the phase start (barrier passed)."""
+    ct = s.chunk_trace.astype(np.int64)
+    n = int((ct[:, 0] > 0).sum())
+    ct = ct[:n]
+    ph_start = tr[0, :, 0]
+    ph_end = tr[0, :, 4]
+    for i, nm in enumerate(names):
+        if not nm.startswith(f"L{mid}."):
+            continue
+        t0 = ph_start[i]
+        sel = [q for q in range(n) if ct[q, 1] >= t0 and ct[q, 1] <= ph_end[i]]
+        print(f"{nm}: staged +{(tr[0, i, 1] - t0) / 1e3:.2f}  chunks-done +{(tr[0, i, 3] - t0) / 1e3:.2f}  "
+              f"end +{(ph_end[i] - t0) / 1e3:.2f} us;  chunks (ready/done): " +
+              " ".join(f"{(ct[q, 1] - t0) / 1e3:.1f}/{(ct[q, 2] - t0) / 1e3:.1f}" for q in sel))
 
 
 if __name__ == "__main__":
