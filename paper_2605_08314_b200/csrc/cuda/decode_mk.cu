@@ -53,6 +53,8 @@ struct Smem {
     uint64_t* dbar;    // [2]
     void* gsh;         // GemvShared
     MkChunk* meta;     // [stages] record of the chunk in each ring slot
+    int* pstart;       // [nph + 1] this CTA's first chunk record of each phase of the launch
+    int* ptiles;       // [nph] first | last << 16 output tile of the CTA's range (-1: none)
 };
 
 // Per-phase shared state of a GEMV phase (computed once, read by all warps).
@@ -62,6 +64,8 @@ struct GemvShared {
     unsigned cnt[kMkMaxLocalTiles];  // chunk completions per local tile (0x10000 = tile complete)
     float inv[4];
     unsigned next;                   // dynamic chunk assignment
+    unsigned ready;                  // warps that published their finalize operands
+    int xpf_ok;                      // xpf holds the residual rows of this CTA's tiles
     int nchunks;                     // this CTA's chunks in the phase
     unsigned released[16];           // rounds of each ring slot consumed so far (whole launch)
     int pos;                         // length register, read once per launch
@@ -93,7 +97,7 @@ __device__ __forceinline__ void finalize_rows(const MkGemv& g, const GemvShared&
                 for (int b = 0; b < B; ++b) {
                     float* xr = g.xres + static_cast<size_t>(b) * g.xres_ld + row;
                     const int pr = row - sh.Tf * kTileRows;  // prefetched residual rows of this CTA
-                    const float x0 = pr < 8 * kTileRows ? sh.xpf[pr * B + b] : __ldcg(xr);
+                    const float x0 = sh.xpf_ok ? sh.xpf[pr * B + b] : __ldcg(xr);
                     const float x = x0 + v[0][b];
                     *xr = x;
                     IO::put(g.out, b, row, x * g.gamma[row]);
@@ -231,22 +235,23 @@ __device__ __forceinline__ bool exchange_pieces(const MkGemv& g, const MkSplit& 
 template <typename W, int B>
 __device__ void gemv_phase(const MkGemv& g, const Smem& sm, GemvShared& sh, int tid, int cta, int G, uint32_t& cseq,
                            uint32_t& xphase, int stages, unsigned long long* tr, unsigned long long* ctr, int chunk_lo,
-                           int chunk_hi, volatile int* prog) {
+                           int chunk_hi, int tinfo, volatile int* prog) {
     constexpr int ES = sizeof(W);
     const int warp = tid >> 5, lane = tid & 31;
-    // ---- stage the input planes (one bulk copy), split, RMSNorm scale,
-    // finalize operands -- all loads in flight together ----
+    // ---- stage the input planes (one bulk copy); the finalize operands (RMSNorm
+    // sum of squares, RoPE row, residual rows) load in the shadow of that copy ----
+    const int Tf = tinfo >= 0 ? (tinfo & 0xFFFF) : 0, Tl = tinfo >= 0 ? (tinfo >> 16) : -1;
     if (tid == 0) {
         const uint32_t xbytes = static_cast<uint32_t>(B) * g.in.len * PlaneIO<W>::kBytesPerElem;
         fence_proxy_async_global();
         mbar_expect_tx(sm.xbar, xbytes);
         bulk_g2s_plain(sm.x, g.in.p, xbytes, sm.xbar);
         sh.sp.init(g.seg, g.nseg, g.dual, ES);
-        sh.ulo = sh.sp.lo(cta, G);
-        sh.uhi = sh.sp.lo(cta + 1, G);
-        sh.Tf = sh.ulo < sh.uhi ? sh.sp.tile_of(sh.ulo) : 0;
+        sh.Tf = Tf;
+        sh.xpf_ok = g.out_kind == kOutResid && Tl >= Tf && (Tl - Tf + 1) * kTileRows <= 8 * kTileRows;
         sh.next = 0u;
         sh.nchunks = chunk_hi - chunk_lo;
+        sh.ready = 0u;
     }
     if (tid < kMkMaxLocalTiles) sh.cnt[tid] = 0u;
     const int rec_per_tile = (g.rec_c0 + g.rec_c1) * kTileRows * B;
@@ -256,21 +261,28 @@ __device__ void gemv_phase(const MkGemv& g, const Smem& sm, GemvShared& sh, int 
         for (int q = tid; q < n4; q += kConsumerThreads) r4[q] = make_float4(0.f, 0.f, 0.f, 0.f);
     }
     consumer_sync();
-    if (g.out_kind == kOutQKV && tid < g.d_head / 2)
-        sh.rope[tid] = g.rope[static_cast<long long>(sh.pos) * (g.d_head / 2) + tid];
-    if (g.out_kind == kOutResid && sh.ulo < sh.uhi) {
-        const int r0 = sh.Tf * kTileRows, nr = (sh.sp.tile_of(sh.uhi - 1) - sh.Tf + 1) * kTileRows;
-        if (nr <= 8 * kTileRows)
-            for (int q = tid; q < nr * B; q += kConsumerThreads) {
-                const int b = q / nr, r = q - b * nr;
-                sh.xpf[r * B + b] = r0 + r < g.seg[0].rows ? __ldcg(g.xres + static_cast<size_t>(b) * g.xres_ld + r0 + r) : 0.f;
-            }
-    }
-    if (g.norm_src) {
-        float ss[B];
+    // issue the operand loads (registers), consumed after the x copy lands
+    float2 rope_v = make_float2(0.f, 0.f);
+    const bool has_rope = g.out_kind == kOutQKV && tid < g.d_head / 2;
+    if (has_rope) rope_v = g.rope[static_cast<long long>(sh.pos) * (g.d_head / 2) + tid];
+    const int nr = (Tl - Tf + 1) * kTileRows;
+    const bool has_xpf = g.out_kind == kOutResid && Tl >= Tf && nr <= 8 * kTileRows;
+    float xpf_v[2] = {0.f, 0.f};
+    if (has_xpf)
 #pragma unroll
-        for (int b = 0; b < B; ++b) {
-            ss[b] = 0.f;
+        for (int u = 0; u < 2; ++u) {
+            const int q = tid + u * kConsumerThreads;
+            if (q < nr * B) {
+                const int b = q / nr, r = q - b * nr, row = Tf * kTileRows + r;
+                xpf_v[u] = row < g.seg[0].rows ? __ldcg(g.xres + static_cast<size_t>(b) * g.xres_ld + row) : 0.f;
+            }
+        }
+    float ss[B];
+#pragma unroll
+    for (int b = 0; b < B; ++b) ss[b] = 0.f;
+    if (g.norm_src)
+#pragma unroll
+        for (int b = 0; b < B; ++b)
             for (int j = tid * 4; j < g.norm_len; j += kConsumerThreads * 4) {
                 const float4 x = __ldcg(reinterpret_cast<const float4*>(g.norm_src + static_cast<size_t>(b) * g.norm_ld + j));
                 ss[b] = fmaf(x.x, x.x, ss[b]);
@@ -278,30 +290,53 @@ __device__ void gemv_phase(const MkGemv& g, const Smem& sm, GemvShared& sh, int 
                 ss[b] = fmaf(x.z, x.z, ss[b]);
                 ss[b] = fmaf(x.w, x.w, ss[b]);
             }
-            ss[b] = warp_sum(ss[b]);
-        }
-        if (lane == 0)
-#pragma unroll
-            for (int b = 0; b < B; ++b) sm.misc[warp * 4 + b] = ss[b];
-        consumer_sync();
-        if (tid < B) {
-            float t = 0.f;
-            for (int w = 0; w < kConsumerWarps; ++w) t += sm.misc[w * 4 + tid];
-            sh.inv[tid] = 1.0f / sqrtf(t / static_cast<float>(g.norm_len) + g.eps);
-        }
-    } else if (tid < B) {
-        sh.inv[tid] = 1.f;
-    }
-    consumer_sync();
     const MkSplit& sp = sh.sp;
-    float inv[B];
-#pragma unroll
-    for (int b = 0; b < B; ++b) inv[b] = sh.inv[b];
     if (prog && tid == 0) prog[1] = 10;
     mbar_wait(sm.xbar, xphase & 1u);
     if (prog && tid == 0) prog[1] = 11;
     ++xphase;
     if (tr && tid == 0) tr[1] = gtimer();
+    // publish the operands; finalizers wait for all 8 warps (sh.ready) before use
+    if (has_rope) sh.rope[tid] = rope_v;
+    if (has_xpf)
+#pragma unroll
+        for (int u = 0; u < 2; ++u) {
+            const int q = tid + u * kConsumerThreads;
+            if (q < nr * B) {
+                const int b = q / nr, r = q - b * nr;
+                sh.xpf[r * B + b] = xpf_v[u];
+            }
+        }
+#pragma unroll
+    for (int b = 0; b < B; ++b) ss[b] = warp_sum(ss[b]);
+    if (lane == 0) {
+#pragma unroll
+        for (int b = 0; b < B; ++b) sm.misc[warp * 4 + b] = ss[b];
+    }
+    __syncwarp();
+    __threadfence_block();
+    if (lane == 0) atomicAdd(&sh.ready, 1u);
+    float inv[B];
+    bool have_inv = false;
+    auto get_inv = [&]() {
+        if (have_inv) return;
+        if (lane == 0)
+            while (*reinterpret_cast<volatile unsigned*>(&sh.ready) < static_cast<unsigned>(kConsumerWarps)) {
+            }
+        __syncwarp();
+        __threadfence_block();
+#pragma unroll
+        for (int b = 0; b < B; ++b) {
+            if (g.norm_src) {
+                float t = 0.f;
+                for (int w = 0; w < kConsumerWarps; ++w) t += *reinterpret_cast<volatile float*>(&sm.misc[w * 4 + b]);
+                inv[b] = 1.0f / sqrtf(t / static_cast<float>(g.norm_len) + g.eps);
+            } else {
+                inv[b] = 1.f;
+            }
+        }
+        have_inv = true;
+    };
 
     // ---- chunks (boundary tiles first): chunk -> warp cseq % 8; the warp that
     // completes a tile's last chunk finalizes the tile right away ----
@@ -371,6 +406,7 @@ __device__ void gemv_phase(const MkGemv& g, const Smem& sm, GemvShared& sh, int 
                 v[sb][b] = acc;
             }
         // (tile-aligned CTA ranges: every tile has exactly one owner, no exchange)
+        get_inv();
         finalize_rows<W, B>(g, sh, T, lane, v, inv);
     }
     if (prog && lane == 0) prog[2 + warp] = 3000000 + nchunks;
@@ -667,6 +703,8 @@ __global__ void __launch_bounds__(kThreads, 1) decode_mk_kernel(const __grid_con
     sm.dbar = reinterpret_cast<uint64_t*>(sm.desc + 2);
     sm.gsh = sm.dbar + 2;
     sm.meta = reinterpret_cast<MkChunk*>(static_cast<char*>(sm.gsh) + (sizeof(GemvShared) + 15) / 16 * 16);
+    sm.pstart = reinterpret_cast<int*>(sm.meta + L.stages);
+    sm.ptiles = sm.pstart + (L.p_end - L.p_begin + 1);
 
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31, cta = blockIdx.x, G = gridDim.x;
     if (tid == 0) {
@@ -736,7 +774,14 @@ __global__ void __launch_bounds__(kThreads, 1) decode_mk_kernel(const __grid_con
     }
     GemvShared& gsh = *static_cast<GemvShared*>(sm.gsh);
     if (tid < 16) gsh.released[tid] = 0u;
-    const int* cst = L.chunk_start + static_cast<size_t>(cta) * (L.nphases + 1);
+    {  // this CTA's rows of the chunk tables, once per launch
+        const int* cs = L.chunk_start + static_cast<size_t>(cta) * (L.nphases + 1) + L.p_begin;
+        const int* ct = L.chunk_tiles + static_cast<size_t>(cta) * L.nphases + L.p_begin;
+        for (int i = tid; i <= L.p_end - L.p_begin; i += kConsumerThreads) {
+            sm.pstart[i] = __ldg(cs + i);
+            if (i < L.p_end - L.p_begin) sm.ptiles[i] = __ldg(ct + i);
+        }
+    }
     if (tid == 0) gsh.pos = L.pos ? __ldcg(L.pos) : 0;  // constant until the argmax phase (last of a step)
     consumer_sync();
     uint32_t cseq = 0, xphase = 0;
@@ -767,7 +812,7 @@ __global__ void __launch_bounds__(kThreads, 1) decode_mk_kernel(const __grid_con
         if (L.progress && tid == 0) L.progress[cta * 16 + 1] = 2;
         const MkPhase& ph = sm.desc[buf];
         switch (ph.kind) {
-            case kMkGemv: gemv_phase<W, B>(ph.g, sm, gsh, tid, cta, G, cseq, xphase, L.stages, tr, tr && cta == 0 ? L.trace + static_cast<size_t>(G) * nph * 16 : nullptr, cst[p], cst[p + 1], L.progress ? L.progress + cta * 16 : nullptr); break;
+            case kMkGemv: gemv_phase<W, B>(ph.g, sm, gsh, tid, cta, G, cseq, xphase, L.stages, tr, tr && cta == 0 ? L.trace + static_cast<size_t>(G) * nph * 16 : nullptr, sm.pstart[idx], sm.pstart[idx + 1], sm.ptiles[idx], L.progress ? L.progress + cta * 16 : nullptr); break;
             case kMkAttn: attn_phase<W, B, DH>(ph.a, sm, tid, cta, G, gsh.pos); break;
             case kMkArgmax: argmax_phase<B>(ph.m, sm, tid, cta); break;
             default: vec_phase<W, B>(ph.v, tid, cta, G); break;
@@ -848,9 +893,10 @@ void mk_split_stats(const GemvSeg* seg, int nseg, int dual, int esize, int grid,
 }
 
 void mk_build_chunks(const MkPhase* phases, int nphases, int grid, int esize, std::vector<MkChunk>& out,
-                     std::vector<int>& start) {
+                     std::vector<int>& start, std::vector<int>& tiles) {
     out.clear();
     start.assign(static_cast<size_t>(grid) * (nphases + 1), 0);
+    tiles.assign(static_cast<size_t>(grid) * nphases, -1);
     for (int c = 0; c < grid; ++c) {
         for (int p = 0; p < nphases; ++p) {
             start[static_cast<size_t>(c) * (nphases + 1) + p] = static_cast<int>(out.size());
@@ -861,6 +907,7 @@ void mk_build_chunks(const MkPhase* phases, int nphases, int grid, int esize, st
             const int ulo = sp.lo(c, grid), uhi = sp.lo(c + 1, grid);
             if (ulo >= uhi) continue;
             const int Tf = sp.tile_of(ulo);
+            tiles[static_cast<size_t>(c) * nphases + p] = Tf | (sp.tile_of(uhi - 1) << 16);
             ChunkSeq cs;
             cs.begin(sp, ulo, uhi);
             int T_prev = -1, ctile = 0;
@@ -898,16 +945,16 @@ static int rec_floats(int rec_chunks, int batch, int d_head) {
     return std::max(rec_chunks * kTileRows * batch, mk::kConsumerWarps * (d_head + 2));
 }
 
-int mk_smem_bytes(int stages, int x_bytes, int rec_chunks, int batch, int d_head) {
+int mk_smem_bytes(int stages, int x_bytes, int rec_chunks, int batch, int d_head, int nphases) {
     return stages * kChunkBytes + mk::mk_barrier_bytes(stages) + x_bytes + rec_floats(rec_chunks, batch, d_head) * 4 +
            256 * 4 + 2 * static_cast<int>(sizeof(MkPhase)) + 16 + static_cast<int>(sizeof(mk::GemvShared)) + 16 +
-           stages * static_cast<int>(sizeof(MkChunk));
+           stages * static_cast<int>(sizeof(MkChunk)) + 8 * (nphases + 1);
 }
 
-int mk_max_stages(int x_bytes, int rec_chunks, int batch, int d_head) {
+int mk_max_stages(int x_bytes, int rec_chunks, int batch, int d_head, int nphases) {
     const int budget = 227 * 1024 - 1024;  // dynamic shared memory per CTA (+ static / alignment slack)
-    int s = (budget - mk_smem_bytes(0, x_bytes, rec_chunks, batch, d_head)) / kChunkBytes;
-    while (s > 0 && mk_smem_bytes(s, x_bytes, rec_chunks, batch, d_head) > budget) --s;
+    int s = (budget - mk_smem_bytes(0, x_bytes, rec_chunks, batch, d_head, nphases)) / kChunkBytes;
+    while (s > 0 && mk_smem_bytes(s, x_bytes, rec_chunks, batch, d_head, nphases) > budget) --s;
     return s;
 }
 

@@ -149,6 +149,7 @@ struct MkLaunch {
     const int* pos;         // length register (constant during a launch but for the final argmax phase)
     const MkChunk* chunks;  // [cta][...] chunk records of every phase
     const int* chunk_start; // [cta][nphases + 1] first record of each phase
+    const int* chunk_tiles; // [cta][nphases] first | last output tile << 16 of the CTA's range (-1: none)
     int nphases;
     volatile int* progress; // optional host-mapped [grid][16] for hang diagnosis
     unsigned long long* trace;  // optional [grid][phases][4] %globaltimer stamps
@@ -169,9 +170,9 @@ void mk_split_stats(const GemvSeg* seg, int nseg, int dual, int esize, int grid,
 constexpr int kMkMaxLocalTiles = 64;
 // Chunk records of every GEMV phase for a grid of `grid` CTAs.
 void mk_build_chunks(const struct MkPhase* phases, int nphases, int grid, int esize, std::vector<MkChunk>& out,
-                     std::vector<int>& start);
-int mk_smem_bytes(int stages, int x_bytes, int rec_chunks, int batch, int d_head);
-int mk_max_stages(int x_bytes, int rec_chunks, int batch, int d_head);
+                     std::vector<int>& start, std::vector<int>& tiles);
+int mk_smem_bytes(int stages, int x_bytes, int rec_chunks, int batch, int d_head, int nphases);
+int mk_max_stages(int x_bytes, int rec_chunks, int batch, int d_head, int nphases);
 int mk_consumer_warps();
 // false if (wt, batch, d_head) has no instantiation
 bool mk_launch(WType wt, int batch, int d_head, const MkLaunch& L, cudaStream_t s);

@@ -690,11 +690,12 @@ void Session::build_program() {
     add_head(x_, 0, ph_pf_argmax_);
 
     const int dh = static_cast<int>(c.d_head);
-    mk_stages_ = std::min(12, k::mk_max_stages(x_bytes_, rec_chunks_, B_, dh));
+    const int nph_all = static_cast<int>(h_phases_.size());
+    mk_stages_ = std::min(12, k::mk_max_stages(x_bytes_, rec_chunks_, B_, dh, nph_all));
     if (mk_stages_ < 2)
         throw ConfigError("decode megakernel: shared memory does not fit this (batch, shape): x " +
                           std::to_string(x_bytes_) + " B, " + std::to_string(rec_chunks_) + " chunk records");
-    mk_smem_ = k::mk_smem_bytes(mk_stages_, x_bytes_, rec_chunks_, B_, dh);
+    mk_smem_ = k::mk_smem_bytes(mk_stages_, x_bytes_, rec_chunks_, B_, dh, nph_all);
     // L2 prefetch distance (chunks per CTA beyond the ring): 16 x 16 KiB x 148 CTAs = 38 MB of the 126 MB L2
     mk_l2_ahead_ = 0;
     if (const char* e = std::getenv("FSVD_MK_L2_AHEAD")) mk_l2_ahead_ = std::max(0, std::atoi(e));
@@ -722,8 +723,10 @@ void Session::build_program() {
         trace_ = static_cast<unsigned long long*>(dalloc(8ull * mk_grid_ * (ph_argmax_ + 1) * 16 + 8ull * 8192 * 4));
     {  // precomputed chunk records of every CTA's weight stream
         std::vector<k::MkChunk> ch;
-        std::vector<int> st;
-        k::mk_build_chunks(h_phases_.data(), static_cast<int>(h_phases_.size()), mk_grid_, m.esize, ch, st);
+        std::vector<int> st, tl;
+        k::mk_build_chunks(h_phases_.data(), static_cast<int>(h_phases_.size()), mk_grid_, m.esize, ch, st, tl);
+        d_chunk_tiles_ = static_cast<int*>(dalloc(sizeof(int) * tl.size()));
+        FSVD_CUDA(cudaMemcpyAsync(d_chunk_tiles_, tl.data(), sizeof(int) * tl.size(), cudaMemcpyHostToDevice, stream_));
         d_chunks_ = static_cast<k::MkChunk*>(dalloc(sizeof(k::MkChunk) * std::max<size_t>(1, ch.size())));
         d_chunk_start_ = static_cast<int*>(dalloc(sizeof(int) * st.size()));
         FSVD_CUDA(cudaMemcpyAsync(d_chunks_, ch.data(), sizeof(k::MkChunk) * ch.size(), cudaMemcpyHostToDevice, stream_));
@@ -750,6 +753,7 @@ void Session::mk_run(int p_begin, int p_end) {
     L.pos = pos_;
     L.chunks = d_chunks_;
     L.chunk_start = d_chunk_start_;
+    L.chunk_tiles = d_chunk_tiles_;
     L.nphases = static_cast<int>(h_phases_.size());
     L.progress = mk_progress_;
     if (trace_ && p_begin == 0 && p_end == ph_argmax_ + 1) L.trace = trace_;

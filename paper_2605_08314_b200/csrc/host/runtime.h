@@ -164,6 +164,7 @@ class Session {
     k::MkPhase* d_phases_ = nullptr;
     k::MkChunk* d_chunks_ = nullptr;
     int* d_chunk_start_ = nullptr;
+    int* d_chunk_tiles_ = nullptr;
     volatile int* mk_progress_ = nullptr;
     int* mk_progress_host_ = nullptr;
     unsigned* mk_bar_ = nullptr;
