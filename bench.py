@@ -351,9 +351,20 @@ def run_ours(args):
             "clocks": clk.summary(),
             "cpu_baseline": cpu,
         }
-        st = sess.stats()
-        kernels_per_token = 9 * L + 3 + (L if sess.resolved()[0] == "no_merge" else 0)
-        line["gpu_launches"] = args.steps * (G * kernels_per_token + (L * 10 + 6))
+        # our kernels in the timed region, per request: prefill = embed + per layer (2 RMSNorm,
+        # 8 tcgen05 GEMMs, 1 flash attention, 2 split-K reductions at prompt 512) + gather + 2
+        # length-register sets + the head/argmax megakernel; decode = one full-step megakernel
+        # launch (one CUDA graph) per token
+        prefill_launches = 1 + L * (2 + 8 + 1 + (2 if P <= 1024 else 0)) + 1 + 2 + 1
+        line["gpu_launches"] = args.steps * (prefill_launches + G * (1 if args.plan == "full_step" else L + 2))
+        tf = ROOT / "profiles" / "traffic.json"
+        if tf.exists():  # dram bytes of one full-step decode launch from an ncu --set full capture
+            try:
+                t = json.loads(tf.read_text())
+                line["roofline"]["traffic"] = t.get("decode_step_dram_bytes")
+                line["roofline"]["traffic_source"] = t.get("source")
+            except Exception:
+                pass
         print(json.dumps(line), flush=True)
     if pg is not None:
         pg.destroy_process_group()
