@@ -40,6 +40,10 @@ namespace mk {
 // full[stages], empty[stages], xbar -- rounded up to 128 B
 __host__ __device__ constexpr int mk_barrier_bytes(int stages) { return ((2 * stages + 1) * 8 + 127) / 128 * 128; }
 
+// attention merge scratch: 3 x [pieces <= grid] floats in the record area
+constexpr int kMaxGrid = 256;
+constexpr int kAttnMergeFloats = 3 * kMaxGrid;
+
 // shared-memory map of one CTA
 struct Smem {
     char* ring;        // [stages][kChunkBytes]
@@ -71,6 +75,7 @@ struct GemvShared {
     int pos;                         // length register, read once per launch
     float2 rope[64];                 // kOutQKV: (cos, sin) of position pos
     float xpf[8 * kTileRows * 4];    // kOutResid: residual rows of the CTA's tiles (<= 8 tiles)
+    float gpf[8 * kTileRows];        // kOutResid: the next RMSNorm's gamma at those rows
 };
 
 // ---------------------------------------------------------------- GEMV ----
@@ -100,7 +105,7 @@ __device__ __forceinline__ void finalize_rows(const MkGemv& g, const GemvShared&
                     const float x0 = sh.xpf_ok ? sh.xpf[pr * B + b] : __ldcg(xr);
                     const float x = x0 + v[0][b];
                     *xr = x;
-                    IO::put(g.out, b, row, x * g.gamma[row]);
+                    IO::put(g.out, b, row, x * (sh.xpf_ok ? sh.gpf[pr] : g.gamma[row]));
                 }
             break;
         case kOutSilu:
@@ -267,7 +272,11 @@ __device__ void gemv_phase(const MkGemv& g, const Smem& sm, GemvShared& sh, int 
     if (has_rope) rope_v = g.rope[static_cast<long long>(sh.pos) * (g.d_head / 2) + tid];
     const int nr = (Tl - Tf + 1) * kTileRows;
     const bool has_xpf = g.out_kind == kOutResid && Tl >= Tf && nr <= 8 * kTileRows;
-    float xpf_v[2] = {0.f, 0.f};
+    float xpf_v[2] = {0.f, 0.f}, gpf_v = 0.f;
+    if (has_xpf && tid < nr) {
+        const int row = Tf * kTileRows + tid;
+        gpf_v = row < g.seg[0].rows ? __ldg(g.gamma + row) : 0.f;
+    }
     if (has_xpf)
 #pragma unroll
         for (int u = 0; u < 2; ++u) {
@@ -282,14 +291,25 @@ __device__ void gemv_phase(const MkGemv& g, const Smem& sm, GemvShared& sh, int 
     for (int b = 0; b < B; ++b) ss[b] = 0.f;
     if (g.norm_src)
 #pragma unroll
-        for (int b = 0; b < B; ++b)
-            for (int j = tid * 4; j < g.norm_len; j += kConsumerThreads * 4) {
-                const float4 x = __ldcg(reinterpret_cast<const float4*>(g.norm_src + static_cast<size_t>(b) * g.norm_ld + j));
-                ss[b] = fmaf(x.x, x.x, ss[b]);
-                ss[b] = fmaf(x.y, x.y, ss[b]);
-                ss[b] = fmaf(x.z, x.z, ss[b]);
-                ss[b] = fmaf(x.w, x.w, ss[b]);
+        for (int b = 0; b < B; ++b) {
+            // all of this thread's loads in flight at once (d <= 8 x 1024)
+            constexpr int kMaxIt = 8;
+            float4 xv[kMaxIt];
+#pragma unroll
+            for (int it = 0; it < kMaxIt; ++it) {
+                const int j = tid * 4 + it * kConsumerThreads * 4;
+                xv[it] = j < g.norm_len
+                             ? __ldcg(reinterpret_cast<const float4*>(g.norm_src + static_cast<size_t>(b) * g.norm_ld + j))
+                             : make_float4(0.f, 0.f, 0.f, 0.f);
             }
+#pragma unroll
+            for (int it = 0; it < kMaxIt; ++it) {
+                ss[b] = fmaf(xv[it].x, xv[it].x, ss[b]);
+                ss[b] = fmaf(xv[it].y, xv[it].y, ss[b]);
+                ss[b] = fmaf(xv[it].z, xv[it].z, ss[b]);
+                ss[b] = fmaf(xv[it].w, xv[it].w, ss[b]);
+            }
+        }
     const MkSplit& sp = sh.sp;
     if (prog && tid == 0) prog[1] = 10;
     mbar_wait(sm.xbar, xphase & 1u);
@@ -298,6 +318,7 @@ __device__ void gemv_phase(const MkGemv& g, const Smem& sm, GemvShared& sh, int 
     if (tr && tid == 0) tr[1] = gtimer();
     // publish the operands; finalizers wait for all 8 warps (sh.ready) before use
     if (has_rope) sh.rope[tid] = rope_v;
+    if (has_xpf && tid < nr) sh.gpf[tid] = gpf_v;
     if (has_xpf)
 #pragma unroll
         for (int u = 0; u < 2; ++u) {
@@ -583,17 +604,39 @@ __device__ void attn_phase(const MkAttn& a, const Smem& sm, int tid, int cta, in
                     while (ld_acquire(a.count + bh) < static_cast<unsigned>(np - 1)) {
                     }
                 consumer_sync();
-                auto pm = [&](int q) { return q < np - 1 ? __ldcg(part + q * ST + DH + 1) : own[DH + 1]; };
-                auto pl = [&](int q) { return q < np - 1 ? __ldcg(part + q * ST + DH) : own[DH]; };
+                // piece maxima / normalizers -> smem in one parallel round of loads
+                // (wst is free: the warp partials are merged into `own`), then the
+                // per-element sums with all pieces' loads in flight; same order as
+                // a serial q loop
+                float* pmv = wst;               // [np]: piece max
+                float* pwv = wst + kMaxGrid;    // [np]: exp(m_q - MM)
+                float* plv = wst + 2 * kMaxGrid;  // [np]: piece normalizer
+                for (int q = tid; q < np; q += kConsumerThreads) {
+                    pmv[q] = q < np - 1 ? __ldcg(part + q * ST + DH + 1) : own[DH + 1];
+                    plv[q] = q < np - 1 ? __ldcg(part + q * ST + DH) : own[DH];
+                }
+                consumer_sync();
                 float MM = -CUDART_INF_F;
-                for (int q = 0; q < np; ++q) MM = fmaxf(MM, pm(q));
+                for (int q = 0; q < np; ++q) MM = fmaxf(MM, pmv[q]);
+                consumer_sync();
+                for (int q = tid; q < np; q += kConsumerThreads) pwv[q] = expf(pmv[q] - MM);
+                consumer_sync();
                 float L = 0.f;
-                for (int q = 0; q < np; ++q) L += pl(q) * expf(pm(q) - MM);
+                for (int q = 0; q < np; ++q) L += plv[q] * pwv[q];
                 const float invL = 1.0f / L;
                 for (int e = tid; e < DH; e += kConsumerThreads) {
                     float o = 0.f;
-                    for (int q = 0; q < np; ++q)
-                        o = fmaf(q < np - 1 ? __ldcg(part + q * ST + e) : own[e], expf(pm(q) - MM), o);
+                    int q = 0;
+                    for (; q + 4 <= np - 1; q += 4) {
+                        const float v0 = __ldcg(part + q * ST + e), v1 = __ldcg(part + (q + 1) * ST + e);
+                        const float v2 = __ldcg(part + (q + 2) * ST + e), v3 = __ldcg(part + (q + 3) * ST + e);
+                        o = fmaf(v0, pwv[q], o);
+                        o = fmaf(v1, pwv[q + 1], o);
+                        o = fmaf(v2, pwv[q + 2], o);
+                        o = fmaf(v3, pwv[q + 3], o);
+                    }
+                    for (; q < np - 1; ++q) o = fmaf(__ldcg(part + q * ST + e), pwv[q], o);
+                    o = fmaf(own[e], pwv[np - 1], o);
                     PlaneIO<W>::put(a.out, b, h * DH + e, o * invL);
                 }
                 if (tid == 0) a.count[bh] = 0u;
@@ -697,7 +740,7 @@ __global__ void __launch_bounds__(kThreads, 1) decode_mk_kernel(const __grid_con
     sm.xbar = sm.empty + L.stages;
     sm.x = reinterpret_cast<char*>(sm.full) + mk_barrier_bytes(L.stages);
     sm.rec = reinterpret_cast<float*>(static_cast<char*>(sm.x) + L.x_bytes);
-    const int rec_floats = std::max(L.rec_chunks * kTileRows * B, kConsumerWarps * (DH + 2));
+    const int rec_floats = std::max({L.rec_chunks * kTileRows * B, kConsumerWarps * (DH + 2), kAttnMergeFloats});
     sm.misc = sm.rec + rec_floats;
     sm.desc = reinterpret_cast<MkPhase*>(sm.misc + 256);
     sm.dbar = reinterpret_cast<uint64_t*>(sm.desc + 2);
@@ -736,18 +779,26 @@ __global__ void __launch_bounds__(kThreads, 1) decode_mk_kernel(const __grid_con
         for (int ib = i0; ib < i1; ib += 32) {
             uint4 rec = make_uint4(0u, 0u, 0u, 0u);
             if (ib + lane < i1) rec = __ldg(reinterpret_cast<const uint4*>(L.chunks + ib + lane));
-            if (L.l2_ahead > 0 && ib + L.l2_ahead + lane < i1) {
-                const MkChunk ahead = L.chunks[ib + L.l2_ahead + lane];
-                prefetch_l2_bulk(ahead.src, static_cast<uint32_t>(ahead.nl & 0xF) * kLineTileBytes);
-            }
+            // L2 prefetch L.l2_ahead chunks beyond the one being issued: HBM keeps
+            // streaming while the ring is full (grid barrier, input staging)
+            uint4 ahd = make_uint4(0u, 0u, 0u, 0u);
+            if (L.l2_ahead > 0 && ib + L.l2_ahead + lane < i1)
+                ahd = __ldg(reinterpret_cast<const uint4*>(L.chunks + ib + L.l2_ahead + lane));
             const int n = min(32, i1 - ib);
             for (int q = 0; q < n; ++q, ++seq) {
-                uint4 r;
+                uint4 r, a;
                 r.x = __shfl_sync(0xffffffffu, rec.x, q);
                 r.y = __shfl_sync(0xffffffffu, rec.y, q);
                 r.z = __shfl_sync(0xffffffffu, rec.z, q);
                 r.w = __shfl_sync(0xffffffffu, rec.w, q);
+                a.x = __shfl_sync(0xffffffffu, ahd.x, q);
+                a.y = __shfl_sync(0xffffffffu, ahd.y, q);
+                a.w = __shfl_sync(0xffffffffu, ahd.w, q);
                 if (lane == 0) {
+                    if (a.x | a.y) {
+                        const MkChunk& ah = *reinterpret_cast<const MkChunk*>(&a);
+                        prefetch_l2_bulk(ah.src, static_cast<uint32_t>(ah.nl & 0xF) * kLineTileBytes);
+                    }
                     const MkChunk& ch = *reinterpret_cast<const MkChunk*>(&r);
                     const uint32_t slot = seq % L.stages;
                     const uint32_t bytes = static_cast<uint32_t>(ch.nl & 0xF) * kLineTileBytes;
@@ -942,7 +993,7 @@ void mk_build_chunks(const MkPhase* phases, int nphases, int grid, int esize, st
 }
 
 static int rec_floats(int rec_chunks, int batch, int d_head) {
-    return std::max(rec_chunks * kTileRows * batch, mk::kConsumerWarps * (d_head + 2));
+    return std::max({rec_chunks * kTileRows * batch, mk::kConsumerWarps * (d_head + 2), mk::kAttnMergeFloats});
 }
 
 int mk_smem_bytes(int stages, int x_bytes, int rec_chunks, int batch, int d_head, int nphases) {

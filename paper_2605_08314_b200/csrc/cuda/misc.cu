@@ -38,6 +38,58 @@ __global__ void rmsnorm_rows_kernel(const float* x, int x_ld, const float* gamma
     for (int i = threadIdx.x; i < d; i += blockDim.x) yr[i] = from_f32<T>(xr[i] * inv * gamma[i]);
 }
 
+// Same op, float4-vectorized with every load of the row in flight at once and
+// the row kept in registers between the two passes (d % 4 == 0, d <= 8192).
+template <typename T>
+__global__ void __launch_bounds__(256) rmsnorm_rows_vec_kernel(const float* x, int x_ld, const float* gamma, float eps,
+                                                               int d, T* y, int y_ld) {
+    constexpr int kIt = 8;
+    __shared__ float red[8];
+    const float4* xr = reinterpret_cast<const float4*>(x + static_cast<long long>(blockIdx.x) * x_ld);
+    const int n4 = d >> 2;
+    float4 v[kIt];
+    float ss = 0.f;
+#pragma unroll
+    for (int it = 0; it < kIt; ++it) {
+        const int i = threadIdx.x + it * 256;
+        v[it] = i < n4 ? xr[i] : make_float4(0.f, 0.f, 0.f, 0.f);
+    }
+#pragma unroll
+    for (int it = 0; it < kIt; ++it) {
+        ss = fmaf(v[it].x, v[it].x, ss);
+        ss = fmaf(v[it].y, v[it].y, ss);
+        ss = fmaf(v[it].z, v[it].z, ss);
+        ss = fmaf(v[it].w, v[it].w, ss);
+    }
+    ss = warp_sum(ss);
+    if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = ss;
+    __syncthreads();
+    float t = 0.f;
+#pragma unroll
+    for (int w = 0; w < 8; ++w) t += red[w];
+    const float inv = 1.0f / sqrtf(t / static_cast<float>(d) + eps);
+    const float4* g4 = reinterpret_cast<const float4*>(gamma);
+    T* yr = y + static_cast<long long>(blockIdx.x) * y_ld;
+#pragma unroll
+    for (int it = 0; it < kIt; ++it) {
+        const int i = threadIdx.x + it * 256;
+        if (i < n4) {
+            const float4 gv = __ldg(g4 + i);
+            const float o0 = v[it].x * inv * gv.x, o1 = v[it].y * inv * gv.y;
+            const float o2 = v[it].z * inv * gv.z, o3 = v[it].w * inv * gv.w;
+            if constexpr (sizeof(T) == 2) {
+                __nv_bfloat162 a = __floats2bfloat162_rn(o0, o1), b = __floats2bfloat162_rn(o2, o3);
+                uint2 u;
+                u.x = *reinterpret_cast<uint32_t*>(&a);
+                u.y = *reinterpret_cast<uint32_t*>(&b);
+                reinterpret_cast<uint2*>(yr)[i] = u;
+            } else {
+                reinterpret_cast<float4*>(yr)[i] = make_float4(o0, o1, o2, o3);
+            }
+        }
+    }
+}
+
 __global__ void gather_last_kernel(const float* x, int x_ld, int T, int d, float* xl, int xl_ld) {
     const int b = blockIdx.y;
     const float* src = x + (static_cast<long long>(b) * T + T - 1) * x_ld;
@@ -127,6 +179,17 @@ void embed(WType wt, const void* emb, int ld_emb, const int* tokens, int n, int 
 
 void rmsnorm_rows(WType wt, const float* x, int x_ld, const float* gamma, float eps, int rows, int d, void* y,
                   int y_ld, cudaStream_t s) {
+    const bool vec = d % 4 == 0 && d <= 8192 && x_ld % 4 == 0 && y_ld % 4 == 0 &&
+                     (reinterpret_cast<uintptr_t>(x) & 15) == 0 && (reinterpret_cast<uintptr_t>(gamma) & 15) == 0 &&
+                     (reinterpret_cast<uintptr_t>(y) & 15) == 0;
+    if (vec) {
+        if (wt == kBF16)
+            rmsnorm_rows_vec_kernel<__nv_bfloat16><<<rows, 256, 0, s>>>(x, x_ld, gamma, eps, d,
+                                                                          static_cast<__nv_bfloat16*>(y), y_ld);
+        else
+            rmsnorm_rows_vec_kernel<float><<<rows, 256, 0, s>>>(x, x_ld, gamma, eps, d, static_cast<float*>(y), y_ld);
+        return;
+    }
     if (wt == kBF16)
         rmsnorm_rows_kernel<__nv_bfloat16><<<rows, 256, 0, s>>>(x, x_ld, gamma, eps, d,
                                                                   static_cast<__nv_bfloat16*>(y), y_ld);
