@@ -488,23 +488,140 @@ struct KvRaw<__nv_bfloat16, 4> {
     }
 };
 
+// Merge of head bh's warp partials (warps [w0, w1) of this CTA): a head held by
+// one CTA is normalized directly into the o-projection's input planes; a head
+// shared by several CTAs goes through per-CTA pieces, merged in CTA order by
+// the CTA holding its newest keys (the others publish with a release
+// increment and never wait).
+template <typename W, int B, int DH>
+__device__ void attn_merge(const MkAttn& a, const Smem& sm, int tid, int cta, int G, const RowSplit& rs, int len, int bh,
+                           int w0, int w1) {
+    constexpr int ST = DH + 2;
+    float* wst = sm.rec;
+    const int b = bh / a.n_heads, h = bh % a.n_heads;
+    const int lo_bh = bh * len, hi_bh = lo_bh + len;
+    const int c0 = rs.cta_of(lo_bh, G), c1 = rs.cta_of(hi_bh - 1, G);
+    const int np = rs.nonempty(c0, c1 + 1, G);
+    float M = -CUDART_INF_F;
+    for (int w = w0; w < w1; ++w) M = fmaxf(M, wst[w * ST + DH + 1]);
+    float* part = a.partial + static_cast<long long>(bh) * a.splits * ST;
+    if (np > 1) {
+        const int slot = rs.nonempty(c0, cta, G);
+        const bool fin = slot == np - 1;
+        float* own = fin ? sm.misc + 96 : part + slot * ST;  // (misc[96..226) is free here)
+        for (int e = tid; e < DH + 1; e += kConsumerThreads) {
+            float t = 0.f;
+            for (int w = w0; w < w1; ++w) {
+                const float mw = wst[w * ST + DH + 1];
+                if (mw != -CUDART_INF_F) t += wst[w * ST + e] * expf(mw - M);
+            }
+            own[e] = t;
+        }
+        if (tid == 0) own[DH + 1] = M;
+        consumer_sync();
+        if (!fin) {
+            if (tid == 0) {
+                fence_acq_rel_gpu();
+                red_release_add(a.count + bh, 1u);
+            }
+        } else {
+            if (tid == 0)
+                while (ld_acquire(a.count + bh) < static_cast<unsigned>(np - 1)) {
+                }
+            consumer_sync();
+            // piece maxima / normalizers -> smem in one parallel round of loads
+            // (wst is free: every warp partial is merged by now), then the
+            // per-element sums with all pieces' loads in flight; same order as
+            // a serial q loop
+            float* pmv = wst;                 // [np]: piece max
+            float* pwv = wst + kMaxGrid;      // [np]: exp(m_q - MM)
+            float* plv = wst + 2 * kMaxGrid;  // [np]: piece normalizer
+            for (int q = tid; q < np; q += kConsumerThreads) {
+                pmv[q] = q < np - 1 ? __ldcg(part + q * ST + DH + 1) : own[DH + 1];
+                plv[q] = q < np - 1 ? __ldcg(part + q * ST + DH) : own[DH];
+            }
+            consumer_sync();
+            float MM = -CUDART_INF_F;
+            for (int q = 0; q < np; ++q) MM = fmaxf(MM, pmv[q]);
+            consumer_sync();
+            for (int q = tid; q < np; q += kConsumerThreads) pwv[q] = expf(pmv[q] - MM);
+            consumer_sync();
+            float L = 0.f;
+            for (int q = 0; q < np; ++q) L += plv[q] * pwv[q];
+            const float invL = 1.0f / L;
+            for (int e = tid; e < DH; e += kConsumerThreads) {
+                float o = 0.f;
+                int q = 0;
+                for (; q + 4 <= np - 1; q += 4) {
+                    const float v0 = __ldcg(part + q * ST + e), v1 = __ldcg(part + (q + 1) * ST + e);
+                    const float v2 = __ldcg(part + (q + 2) * ST + e), v3 = __ldcg(part + (q + 3) * ST + e);
+                    o = fmaf(v0, pwv[q], o);
+                    o = fmaf(v1, pwv[q + 1], o);
+                    o = fmaf(v2, pwv[q + 2], o);
+                    o = fmaf(v3, pwv[q + 3], o);
+                }
+                for (; q < np - 1; ++q) o = fmaf(__ldcg(part + q * ST + e), pwv[q], o);
+                o = fmaf(own[e], pwv[np - 1], o);
+                PlaneIO<W>::put(a.out, b, h * DH + e, o * invL);
+            }
+            if (tid == 0) a.count[bh] = 0u;
+        }
+    } else {
+        float L = 0.f;
+        for (int w = w0; w < w1; ++w) {
+            const float mw = wst[w * ST + DH + 1];
+            if (mw != -CUDART_INF_F) L += wst[w * ST + DH] * expf(mw - M);
+        }
+        const float invL = 1.0f / L;
+        for (int e = tid; e < DH; e += kConsumerThreads) {
+            float t = 0.f;
+            for (int w = w0; w < w1; ++w) {
+                const float mw = wst[w * ST + DH + 1];
+                if (mw != -CUDART_INF_F) t += wst[w * ST + e] * expf(mw - M);
+            }
+            PlaneIO<W>::put(a.out, b, h * DH + e, t * invL);
+        }
+    }
+    consumer_sync();
+}
+
+// Dense-KV decode attention (online softmax math.hpp:56-101).
+// The B*H*len key rows are split evenly over the CTAs. A CTA works on its
+// heads two at a time (with B*H < grid it never has more than two), the warps
+// split between them in proportion to their rows, so a CTA straddling a head
+// boundary takes no longer than one inside a head. Each warp streams its rows
+// 16 at a time (all of a batch's K/V loads in flight), then the heads are
+// merged, the one shared with the next CTA first (publish, no wait).
 template <typename W, int B, int DH>
 __device__ void attn_phase(const MkAttn& a, const Smem& sm, int tid, int cta, int G, int pos) {
-    constexpr int PER = DH / 32, KU = 8, ST = DH + 2;
+    constexpr int PER = DH / 32, KU = 16, ST = DH + 2;
     const int warp = tid >> 5, lane = tid & 31;
     const int len = pos + 1;
     RowSplit rs{B * a.n_heads * len};
     const int r0 = rs.lo(cta, G), r1 = rs.lo(cta + 1, G);
+    if (r1 <= r0) return;
     float* wst = sm.rec;  // [warps][DH + 2]: acc, l, m
-    // heads in reverse: a CTA publishes its share of the head it shares with
-    // the next CTA first, then finalizes the heads whose newest keys it holds
-    // (their other contributors published first too) -- no wait chains
-    const int bh_first = r0 / len, bh_last = r1 > r0 ? (r1 - 1) / len : bh_first - 1;
-    for (int bh = bh_last; bh >= bh_first; --bh) {
-        const int lo_bh = bh * len, hi_bh = lo_bh + len;
-        const int j0 = static_cast<int>((r0 > lo_bh ? r0 : lo_bh) - lo_bh);
-        const int j1 = static_cast<int>((r1 < hi_bh ? r1 : hi_bh) - lo_bh);
-        if (j1 <= j0) continue;
+    const int bh_first = r0 / len, bh_last = (r1 - 1) / len;
+    for (int bh_hi = bh_last; bh_hi >= bh_first; bh_hi -= 2) {
+        const int bh_lo = max(bh_first, bh_hi - 1);
+        auto span = [&](int bh, int& j0, int& j1) {
+            const int lo_bh = bh * len, hi_bh = lo_bh + len;
+            j0 = (r0 > lo_bh ? r0 : lo_bh) - lo_bh;
+            j1 = (r1 < hi_bh ? r1 : hi_bh) - lo_bh;
+        };
+        int jl0, jl1, jh0, jh1;
+        span(bh_lo, jl0, jl1);
+        span(bh_hi, jh0, jh1);
+        int w_lo = 0;  // warps [0, w_lo) on bh_lo, [w_lo, 8) on bh_hi
+        if (bh_lo != bh_hi) {
+            const int nl = jl1 - jl0, nh = jh1 - jh0;
+            w_lo = (2 * kConsumerWarps * nl + (nl + nh)) / (2 * (nl + nh));  // round(8 nl / (nl + nh))
+            w_lo = min(max(w_lo, 1), kConsumerWarps - 1);
+        }
+        const bool on_lo = warp < w_lo;
+        const int bh = on_lo ? bh_lo : bh_hi;
+        const int j0 = on_lo ? jl0 : jh0, j1 = on_lo ? jl1 : jh1;
+        const int wi = on_lo ? warp : warp - w_lo, nw = on_lo ? w_lo : kConsumerWarps - w_lo;
         const int b = bh / a.n_heads, h = bh % a.n_heads;
         const W* Kc = static_cast<const W*>(a.kcache) + b * a.cache_bstride + h * a.cache_hstride;
         const W* Vc = static_cast<const W*>(a.vcache) + b * a.cache_bstride + h * a.cache_hstride;
@@ -514,39 +631,29 @@ __device__ void attn_phase(const MkAttn& a, const Smem& sm, int tid, int cta, in
 #pragma unroll
             for (int e = 0; e < PER; ++e) qr[e] = __ldcg(q + e) * a.scale;
         }
-        // this warp's keys
         const int n = j1 - j0;
-        const int k0 = j0 + n * warp / kConsumerWarps, k1 = j0 + n * (warp + 1) / kConsumerWarps;
+        const int k0 = j0 + n * wi / nw, k1 = j0 + n * (wi + 1) / nw;
         float m = -CUDART_INF_F, l = 0.f, acc[PER];
 #pragma unroll
         for (int e = 0; e < PER; ++e) acc[e] = 0.f;
-        // software pipeline: the next batch of KU keys is in flight while this one is reduced
         using Raw = typename KvRaw<W, PER>::T;
-        Raw kraw[KU], vraw[KU];
-        auto load_batch = [&](int kb, Raw (&kq)[KU], Raw (&vq)[KU]) {
+        for (int kb = k0; kb < k1; kb += KU) {
+            Raw kq[KU], vq[KU];
 #pragma unroll
             for (int u = 0; u < KU; ++u) {
                 const int jj = min(kb + u, k1 - 1);  // clamp: duplicate loads are masked below
                 kq[u] = KvRaw<W, PER>::load(Kc + static_cast<long long>(jj) * DH + lane * PER);
                 vq[u] = KvRaw<W, PER>::load(Vc + static_cast<long long>(jj) * DH + lane * PER);
             }
-        };
-        if (k0 < k1) load_batch(k0, kraw, vraw);
-        for (int kb = k0; kb < k1; kb += KU) {
-            float kr[KU][PER], vr[KU][PER];
-#pragma unroll
-            for (int u = 0; u < KU; ++u) {
-                KvRaw<W, PER>::unpack(kraw[u], kr[u]);
-                KvRaw<W, PER>::unpack(vraw[u], vr[u]);
-            }
-            if (kb + KU < k1) load_batch(kb + KU, kraw, vraw);
             float sc[KU];
             float mb = -CUDART_INF_F;
 #pragma unroll
             for (int u = 0; u < KU; ++u) {
+                float kr[PER];
+                KvRaw<W, PER>::unpack(kq[u], kr);
                 float d = 0.f;
 #pragma unroll
-                for (int e = 0; e < PER; ++e) d = fmaf(qr[e], kr[u][e], d);
+                for (int e = 0; e < PER; ++e) d = fmaf(qr[e], kr[e], d);
                 d = warp_sum(d);
                 sc[u] = kb + u < k1 ? d : -CUDART_INF_F;
                 mb = fmaxf(mb, sc[u]);
@@ -558,10 +665,12 @@ __device__ void attn_phase(const MkAttn& a, const Smem& sm, int tid, int cta, in
             for (int e = 0; e < PER; ++e) acc[e] *= r;
 #pragma unroll
             for (int u = 0; u < KU; ++u) {
+                float vr[PER];
+                KvRaw<W, PER>::unpack(vq[u], vr);
                 const float w = expf(sc[u] - mn);
                 l += w;
 #pragma unroll
-                for (int e = 0; e < PER; ++e) acc[e] = fmaf(w, vr[u][e], acc[e]);
+                for (int e = 0; e < PER; ++e) acc[e] = fmaf(w, vr[e], acc[e]);
             }
             m = mn;
         }
@@ -572,92 +681,12 @@ __device__ void attn_phase(const MkAttn& a, const Smem& sm, int tid, int cta, in
             wst[warp * ST + DH + 1] = m;
         }
         consumer_sync();
-        // CTA partial (warps merged in order) -> pieces or direct
-        const int c0 = rs.cta_of(lo_bh, G), c1 = rs.cta_of(hi_bh - 1, G);
-        const int np = rs.nonempty(c0, c1 + 1, G);
-        float M = -CUDART_INF_F;
-        for (int w = 0; w < kConsumerWarps; ++w) M = fmaxf(M, wst[w * ST + DH + 1]);
-        float* part = a.partial + static_cast<long long>(bh) * a.splits * ST;
-        if (np > 1) {
-            // Shared head: the CTA holding the newest keys (slot np-1) finalizes;
-            // the others publish their partial with a release increment (no wait).
-            const int slot = rs.nonempty(c0, cta, G);
-            const bool fin = slot == np - 1;
-            float* own = fin ? sm.misc + 96 : part + slot * ST;  // (misc[96..226) is free here)
-            for (int e = tid; e < DH + 1; e += kConsumerThreads) {
-                float t = 0.f;
-                for (int w = 0; w < kConsumerWarps; ++w) {
-                    const float mw = wst[w * ST + DH + 1];
-                    if (mw != -CUDART_INF_F) t += wst[w * ST + e] * expf(mw - M);
-                }
-                own[e] = t;
-            }
-            if (tid == 0) own[DH + 1] = M;
-            consumer_sync();
-            if (!fin) {
-                if (tid == 0) {
-                    fence_acq_rel_gpu();
-                    red_release_add(a.count + bh, 1u);
-                }
-            } else {
-                if (tid == 0)
-                    while (ld_acquire(a.count + bh) < static_cast<unsigned>(np - 1)) {
-                    }
-                consumer_sync();
-                // piece maxima / normalizers -> smem in one parallel round of loads
-                // (wst is free: the warp partials are merged into `own`), then the
-                // per-element sums with all pieces' loads in flight; same order as
-                // a serial q loop
-                float* pmv = wst;               // [np]: piece max
-                float* pwv = wst + kMaxGrid;    // [np]: exp(m_q - MM)
-                float* plv = wst + 2 * kMaxGrid;  // [np]: piece normalizer
-                for (int q = tid; q < np; q += kConsumerThreads) {
-                    pmv[q] = q < np - 1 ? __ldcg(part + q * ST + DH + 1) : own[DH + 1];
-                    plv[q] = q < np - 1 ? __ldcg(part + q * ST + DH) : own[DH];
-                }
-                consumer_sync();
-                float MM = -CUDART_INF_F;
-                for (int q = 0; q < np; ++q) MM = fmaxf(MM, pmv[q]);
-                consumer_sync();
-                for (int q = tid; q < np; q += kConsumerThreads) pwv[q] = expf(pmv[q] - MM);
-                consumer_sync();
-                float L = 0.f;
-                for (int q = 0; q < np; ++q) L += plv[q] * pwv[q];
-                const float invL = 1.0f / L;
-                for (int e = tid; e < DH; e += kConsumerThreads) {
-                    float o = 0.f;
-                    int q = 0;
-                    for (; q + 4 <= np - 1; q += 4) {
-                        const float v0 = __ldcg(part + q * ST + e), v1 = __ldcg(part + (q + 1) * ST + e);
-                        const float v2 = __ldcg(part + (q + 2) * ST + e), v3 = __ldcg(part + (q + 3) * ST + e);
-                        o = fmaf(v0, pwv[q], o);
-                        o = fmaf(v1, pwv[q + 1], o);
-                        o = fmaf(v2, pwv[q + 2], o);
-                        o = fmaf(v3, pwv[q + 3], o);
-                    }
-                    for (; q < np - 1; ++q) o = fmaf(__ldcg(part + q * ST + e), pwv[q], o);
-                    o = fmaf(own[e], pwv[np - 1], o);
-                    PlaneIO<W>::put(a.out, b, h * DH + e, o * invL);
-                }
-                if (tid == 0) a.count[bh] = 0u;
-            }
+        if (bh_lo != bh_hi) {
+            attn_merge<W, B, DH>(a, sm, tid, cta, G, rs, len, bh_hi, w_lo, kConsumerWarps);
+            attn_merge<W, B, DH>(a, sm, tid, cta, G, rs, len, bh_lo, 0, w_lo);
         } else {
-            float L = 0.f;
-            for (int w = 0; w < kConsumerWarps; ++w) {
-                const float mw = wst[w * ST + DH + 1];
-                if (mw != -CUDART_INF_F) L += wst[w * ST + DH] * expf(mw - M);
-            }
-            const float invL = 1.0f / L;
-            for (int e = tid; e < DH; e += kConsumerThreads) {
-                float t = 0.f;
-                for (int w = 0; w < kConsumerWarps; ++w) {
-                    const float mw = wst[w * ST + DH + 1];
-                    if (mw != -CUDART_INF_F) t += wst[w * ST + e] * expf(mw - M);
-                }
-                PlaneIO<W>::put(a.out, b, h * DH + e, t * invL);
-            }
+            attn_merge<W, B, DH>(a, sm, tid, cta, G, rs, len, bh_hi, 0, kConsumerWarps);
         }
-        consumer_sync();
     }
 }
 

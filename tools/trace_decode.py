@@ -91,6 +91,14 @@ def main():
         if n.startswith(f"L{mid}.") or n == "head":
             print(f"{n:10s} {f_sum[i]:6.2f} {f_fence[i]:6.2f} {f_atom[i]:6.2f} {f_load[i]:6.2f} {f_rows[i]:6.2f} {f_tail[i]:6.2f}")
     spans = end - start
+    ia = names.index(f"L{mid}.attn") if f"L{mid}.attn" in names else None
+    if ia is not None:
+        d = (tr[:, ia, 4] - tr[:, ia, 0]) / 1e3
+        st = (tr[:, ia, 0] - tr[:, ia, 0].min()) / 1e3
+        order = np.argsort(-d)
+        print("attention phase, slowest CTAs: cta dur start_offset")
+        print("  " + " ".join(f"{c}:{d[c]:.2f}/{st[c]:.2f}" for c in order[:30]))
+        print("  fastest: " + " ".join(f"{c}:{d[c]:.2f}" for c in order[-10:]))
     cta0_timeline(s, tr, names, mid)
     print(f"sum: stage {stage.sum():.1f} us, chunks {chunks.sum():.1f} us, finalize {fin.sum():.1f} us, "
           f"phase spans {spans.sum() / 1e3:.1f} us")
