@@ -252,6 +252,25 @@ __device__ void gemv_phase(const MkGemv& g, const Smem& sm, GemvShared& sh, int 
         mbar_expect_tx(sm.xbar, xbytes);
         bulk_g2s_plain(sm.x, g.in.p, xbytes, sm.xbar);
         sh.sp.init(g.seg, g.nseg, g.dual, ES);
+        if (g.out_kind == kOutQKV) {
+            // warm L2 with the K/V rows this CTA reads in the attention phase that
+            // follows (rows < pos are final; row pos is appended by this phase)
+            const int H = g.seg[0].rows / g.d_head, len = sh.pos + 1;
+            const RowSplit rs{B * H * len};
+            const int r0 = rs.lo(cta, G), r1 = rs.lo(cta + 1, G);
+            for (int bh = r0 / len; r1 > r0 && bh <= (r1 - 1) / len; ++bh) {
+                const int j0 = max(r0 - bh * len, 0), j1 = min(r1 - bh * len, len - 1);
+                if (j1 <= j0) continue;
+                const long long off = (bh / H) * g.cache_bstride + (bh % H) * g.cache_hstride +
+                                      static_cast<long long>(j0) * g.d_head;
+                const uint32_t bytes = static_cast<uint32_t>(j1 - j0) * g.d_head * ES;
+                for (uint32_t o = 0; o < bytes; o += 16384u) {
+                    const uint32_t n = min(16384u, bytes - o);
+                    prefetch_l2_bulk(static_cast<const char*>(g.kcache) + off * ES + o, n);
+                    prefetch_l2_bulk(static_cast<const char*>(g.vcache) + off * ES + o, n);
+                }
+            }
+        }
         sh.Tf = Tf;
         sh.xpf_ok = g.out_kind == kOutResid && Tl >= Tf && (Tl - Tf + 1) * kTileRows <= 8 * kTileRows;
         sh.next = 0u;
@@ -529,40 +548,34 @@ __device__ void attn_merge(const MkAttn& a, const Smem& sm, int tid, int cta, in
                 while (ld_acquire(a.count + bh) < static_cast<unsigned>(np - 1)) {
                 }
             consumer_sync();
-            // piece maxima / normalizers -> smem in one parallel round of loads
-            // (wst is free: every warp partial is merged by now), then the
-            // per-element sums with all pieces' loads in flight; same order as
-            // a serial q loop
-            float* pmv = wst;                 // [np]: piece max
-            float* pwv = wst + kMaxGrid;      // [np]: exp(m_q - MM)
-            float* plv = wst + 2 * kMaxGrid;  // [np]: piece normalizer
-            for (int q = tid; q < np; q += kConsumerThreads) {
-                pmv[q] = q < np - 1 ? __ldcg(part + q * ST + DH + 1) : own[DH + 1];
-                plv[q] = q < np - 1 ? __ldcg(part + q * ST + DH) : own[DH];
-            }
-            consumer_sync();
-            float MM = -CUDART_INF_F;
-            for (int q = 0; q < np; ++q) MM = fmaxf(MM, pmv[q]);
-            consumer_sync();
-            for (int q = tid; q < np; q += kConsumerThreads) pwv[q] = expf(pmv[q] - MM);
-            consumer_sync();
-            float L = 0.f;
-            for (int q = 0; q < np; ++q) L += plv[q] * pwv[q];
-            const float invL = 1.0f / L;
-            for (int e = tid; e < DH; e += kConsumerThreads) {
-                float o = 0.f;
-                int q = 0;
-                for (; q + 4 <= np - 1; q += 4) {
-                    const float v0 = __ldcg(part + q * ST + e), v1 = __ldcg(part + (q + 1) * ST + e);
-                    const float v2 = __ldcg(part + (q + 2) * ST + e), v3 = __ldcg(part + (q + 3) * ST + e);
-                    o = fmaf(v0, pwv[q], o);
-                    o = fmaf(v1, pwv[q + 1], o);
-                    o = fmaf(v2, pwv[q + 2], o);
-                    o = fmaf(v3, pwv[q + 3], o);
+            // one round of loads: every piece's (m, l, acc[e]) in flight at once,
+            // then an online merge in CTA order (running max, rescaled sums)
+            if (tid < DH) {
+                const int e = tid;
+                constexpr int QB = 8;
+                float MM = -CUDART_INF_F, L = 0.f, o = 0.f;
+                auto fold = [&](float mq, float lq, float aq) {
+                    const float mn = fmaxf(MM, mq);
+                    const float so = expf(MM - mn), sq = expf(mq - mn);
+                    L = fmaf(L, so, lq * sq);
+                    o = fmaf(o, so, aq * sq);
+                    MM = mn;
+                };
+                for (int q0 = 0; q0 < np - 1; q0 += QB) {
+                    float mv[QB], lv[QB], av[QB];
+#pragma unroll
+                    for (int u = 0; u < QB; ++u) {
+                        const int q = min(q0 + u, np - 2);
+                        mv[u] = __ldcg(part + q * ST + DH + 1);
+                        lv[u] = __ldcg(part + q * ST + DH);
+                        av[u] = __ldcg(part + q * ST + e);
+                    }
+#pragma unroll
+                    for (int u = 0; u < QB; ++u)
+                        if (q0 + u < np - 1) fold(mv[u], lv[u], av[u]);
                 }
-                for (; q < np - 1; ++q) o = fmaf(__ldcg(part + q * ST + e), pwv[q], o);
-                o = fmaf(own[e], pwv[np - 1], o);
-                PlaneIO<W>::put(a.out, b, h * DH + e, o * invL);
+                fold(own[DH + 1], own[DH], own[e]);
+                PlaneIO<W>::put(a.out, b, h * DH + e, o / L);
             }
             if (tid == 0) a.count[bh] = 0u;
         }
