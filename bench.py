@@ -36,6 +36,21 @@ sys.path.insert(0, str(ROOT))
 PROMPT, GEN, BATCH = 512, 256, 1
 FAMILY, RHO, SEED = "A", 0.6, 1
 
+# BASELINE.json configs: model preset, factorization family,
+# prompt, decode horizon, batch per GPU. c2 is the headline; the others are
+# measured with --config for the record (the batched engine serves B > 2).
+CONFIGS = {
+    "c2": dict(model="llama7b", family="A", prompt=512, gen=256, batch=1,
+               desc="C2: LLaMA-7B-shape SVD-LLM v1 (family A) rho=0.6, prompt 512, decode 256, batch 1"),
+    "c3": dict(model="llama7b", family="C", prompt=2048, gen=512, batch=8,
+               desc="C3: LLaMA-7B-shape Basis-Sharing (family C, groups of 2) rho=0.6, prompt 2048, decode 512, batch 8"),
+    "c4": dict(model="llama13b", family="D", prompt=512, gen=4096, batch=16,
+               desc="C4: LLaMA-13B-shape activation-truncated (family D) rho=0.6, prompt 512, decode 4096, batch 16"),
+    "c5": dict(model="llama7b", family="B", prompt=1024, gen=256, batch=32,
+               desc="C5: LLaMA-7B-shape SVD-LLM v2 (family B) rho=0.6, 256 requests as waves of 32 per GPU, "
+                    "prompt 1024, decode 256"),
+}
+
 
 def parse():
     p = argparse.ArgumentParser()
@@ -43,13 +58,23 @@ def parse():
     p.add_argument("--steps", type=int, default=3)
     p.add_argument("--warmup", type=int, default=3)
     p.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    p.add_argument("--prompt", type=int, default=PROMPT)
-    p.add_argument("--gen", type=int, default=GEN)
-    p.add_argument("--batch", type=int, default=BATCH)
+    p.add_argument("--config", default="c2", choices=sorted(CONFIGS))
+    p.add_argument("--prompt", type=int, default=None)
+    p.add_argument("--gen", type=int, default=None)
+    p.add_argument("--batch", type=int, default=None)
     p.add_argument("--plan", default="full_step", choices=["eager", "per_layer", "full_step"])
     p.add_argument("--no-cpu-baseline", action="store_true")
     p.add_argument("--cpu-steps", type=int, default=6, help="decode steps in the bounded CPU sample")
-    return p.parse_args()
+    a = p.parse_args()
+    c = CONFIGS[a.config]
+    a.prompt = c["prompt"] if a.prompt is None else a.prompt
+    a.gen = c["gen"] if a.gen is None else a.gen
+    a.batch = c["batch"] if a.batch is None else a.batch
+    a.model, a.family = c["model"], c["family"]
+    a.workload = c["desc"]
+    if (a.prompt, a.gen, a.batch) != (c["prompt"], c["gen"], c["batch"]):
+        a.workload += f" [overridden: prompt {a.prompt}, decode {a.gen}, batch {a.batch}]"
+    return a
 
 
 def peaks():
@@ -138,9 +163,9 @@ def barrier(pg):
         torch.cuda.synchronize()
 
 
-def spec_c2(fsvd, prompt, gen):
-    cfg, _ = fsvd.PRESETS["llama7b"]
-    return fsvd.SynthSpec(cfg, capacity=max(1024, prompt + gen + 64), family=FAMILY, rho=RHO, seed=SEED)
+def spec_c2(fsvd, prompt, gen, model="llama7b", family=FAMILY):
+    cfg, _ = fsvd.PRESETS[model]
+    return fsvd.SynthSpec(cfg, capacity=max(1024, prompt + gen + 64), family=family, rho=RHO, seed=SEED)
 
 
 # ------------------------------------------------------------- CPU baseline --
@@ -220,7 +245,7 @@ def run_ours(args):
     import paper_2605_08314_b200 as fsvd
 
     hbm, tf_burst, tf_sust, peak_src = peaks()
-    spec = spec_c2(fsvd, args.prompt, args.gen)
+    spec = spec_c2(fsvd, args.prompt, args.gen, args.model, args.family)
     B, P, G = args.batch, args.prompt, args.gen
     model = fsvd.Model.synthetic(spec, dtype="bf16", device=local)
     info = model.info()
@@ -295,20 +320,21 @@ def run_ours(args):
         ip = ctypes.POINTER(ctypes.c_int32)
         fp = ctypes.POINTER(ctypes.c_float)
         e2e_dec = []
+        Ge = min(G, 256)  # host-API decode steps timed per repetition (the whole horizon up to 256)
         for rep in range(max(1, min(args.steps, 2)) + 1):
             sess.reset()
             fsvd._check(L_.fsvd_prefill(sess._h, ctypes.cast(hp.data_ptr(), ip), P, ctypes.cast(logits.data_ptr(), fp)))
             tok.copy_(logits.argmax(dim=1).to(torch.int32))
             t0 = time.perf_counter()
-            for _ in range(G):
+            for _ in range(Ge):
                 fsvd._check(L_.fsvd_decode_step(sess._h, ctypes.cast(tok.data_ptr(), ip),
                                                 ctypes.cast(logits.data_ptr(), fp)))
                 tok.copy_(logits.argmax(dim=1).to(torch.int32))
             if rep > 0:
                 e2e_dec.append(time.perf_counter() - t0)
         e2e_s = max_over_ranks(pg, sum(e2e_dec) / len(e2e_dec))
-        e2e = {"value": world * B * G / e2e_s, "unit": "tok/s",
-               "h2d_bytes_per_step": B * 4 * G, "d2h_bytes_per_step": B * cfg.vocab * 4 * G,
+        e2e = {"value": world * B * Ge / e2e_s, "unit": "tok/s",
+               "h2d_bytes_per_step": B * 4 * Ge, "d2h_bytes_per_step": B * cfg.vocab * 4 * Ge,
                "note": "fsvd_decode_step host API per token (pinned host token in, host logits out, host argmax)"}
 
     cpu = None
@@ -333,8 +359,8 @@ def run_ours(args):
             "vs_baseline": None,
             "dtype": "bf16",
             "data": "synthetic (device-generated seeded random-init factors)",
-            "config": {"workload": "C2: LLaMA-7B-shape SVD-LLM v1 (family A) rho=0.6, prompt 512, decode 256, batch 1",
-                       "model": "llama7b-shape", "family": FAMILY, "rho": RHO, "global_batch": B * world,
+            "config": {"workload": args.workload,
+                       "model": f"{args.model}-shape", "family": args.family, "rho": RHO, "global_batch": B * world,
                        "prompt": P, "gen": G, "plan": args.plan, "parallelism": f"replicas x{world}",
                        "l2": "weights 8.3 GB > 126 MB L2: no flush needed"},
             "engine": engine,
@@ -355,8 +381,15 @@ def run_ours(args):
         # 8 tcgen05 GEMMs, 1 flash attention, 2 split-K reductions at prompt 512) + gather + 2
         # length-register sets + the head/argmax megakernel; decode = one full-step megakernel
         # launch (one CUDA graph) per token
-        prefill_launches = 1 + L * (2 + 8 + 1 + (2 if P <= 1024 else 0)) + 1 + 2 + 1
-        line["gpu_launches"] = args.steps * (prefill_launches + G * (1 if args.plan == "full_step" else L + 2))
+        if engine.get("batched"):
+            # batched engine: prefill as above with the head as norm + GEMM + argmax + advance
+            # (5 launches); decode per token = embed + per layer (2 RMSNorm, 8 GEMMs, <= 6
+            # split-K reductions, 1 attention) + head (5), replayed as one graph
+            prefill_launches = 1 + L * (2 + 8 + 1 + (2 if P <= 1024 else 0)) + 1 + 2 + 5
+            line["gpu_launches"] = args.steps * (prefill_launches + G * (1 + L * 17 + 5))
+        else:
+            prefill_launches = 1 + L * (2 + 8 + 1 + (2 if P <= 1024 else 0)) + 1 + 2 + 1
+            line["gpu_launches"] = args.steps * (prefill_launches + G * (1 if args.plan == "full_step" else L + 2))
         tf = ROOT / "profiles" / "traffic.json"
         if tf.exists():  # dram bytes of one full-step decode launch from an ncu --set full capture
             try:

@@ -454,8 +454,9 @@ class Session:
     def engine(self) -> dict:
         v = [C.c_int32() for _ in range(4)]
         _check(lib().fsvd_session_engine(self._h, *[C.byref(x) for x in v]))
-        return {"megakernel": bool(v[0].value), "stage_bytes": v[1].value, "stages": v[2].value,
-                "attn_splits": v[3].value}
+        # kind 1: persistent decode megakernel (B <= 2); 2: batched layer engine
+        return {"megakernel": v[0].value == 1, "batched": v[0].value == 2, "stage_bytes": v[1].value,
+                "stages": v[2].value, "attn_splits": v[3].value}
 
     def trace(self, max_phases: int = 4096) -> np.ndarray:
         """[grid, phases, 8] ns stamps of the last traced full step (FSVD_TRACE=1)."""

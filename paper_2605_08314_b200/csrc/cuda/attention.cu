@@ -18,6 +18,7 @@ constexpr int kPK = 64;        // keys per tile
 constexpr int kPThreads = 256; // 4 threads per query
 template <typename T, int DH>
 __global__ void __launch_bounds__(kPThreads) attn_prefill_kernel(const __grid_constant__ AttnPrefillArgs a) {
+    const int p0 = a.p0_dev ? *a.p0_dev : a.p0;
     extern __shared__ float sm[];
     constexpr int dh = DH;
     float* Ks = sm;                 // [kPK][dh + 1]
@@ -27,7 +28,7 @@ __global__ void __launch_bounds__(kPThreads) attn_prefill_kernel(const __grid_co
     constexpr int slice = DH / 4;  // dims owned by this thread
     const int t = qt * kPQ + qi;
     const bool active = t < a.T;
-    const int qpos = a.p0 + t;
+    const int qpos = p0 + t;
 
     float qv[slice], acc[slice];
     const T* qrow = static_cast<const T*>(a.q) + static_cast<long long>(b * a.T + (active ? t : 0)) * a.q_ld + h * dh;
@@ -41,7 +42,7 @@ __global__ void __launch_bounds__(kPThreads) attn_prefill_kernel(const __grid_co
     const T* K = static_cast<const T*>(a.kcache) + b * a.cache_bstride + h * a.cache_hstride;
     const T* V = static_cast<const T*>(a.vcache) + b * a.cache_bstride + h * a.cache_hstride;
     const int last_q = min(a.T, (qt + 1) * kPQ) - 1;
-    const int kend = a.p0 + last_q + 1;  // keys needed by this CTA
+    const int kend = p0 + last_q + 1;  // keys needed by this CTA
     float sc[kPK];
     for (int k0 = 0; k0 < kend; k0 += kPK) {
         __syncthreads();
@@ -128,6 +129,7 @@ __device__ __forceinline__ uint32_t pack_bf16x2(float lo, float hi) {
 
 template <int DH>
 __global__ void __launch_bounds__(kFThreads) attn_prefill_tc_kernel(const __grid_constant__ AttnPrefillArgs a) {
+    const int p0 = a.p0_dev ? *a.p0_dev : a.p0;
     constexpr int LD = DH + 8;  // padded smem row (bf16): conflict-free ldmatrix
     extern __shared__ __align__(128) __nv_bfloat16 fsm[];
     __nv_bfloat16* Qs = fsm;                 // [kFQ][LD]
@@ -140,7 +142,7 @@ __global__ void __launch_bounds__(kFThreads) attn_prefill_tc_kernel(const __grid
     const __nv_bfloat16* K = static_cast<const __nv_bfloat16*>(a.kcache) + b * a.cache_bstride + h * a.cache_hstride;
     const __nv_bfloat16* V = static_cast<const __nv_bfloat16*>(a.vcache) + b * a.cache_bstride + h * a.cache_hstride;
     const int last_q = min(a.T, q0 + kFQ) - 1;
-    const int kend = a.p0 + last_q + 1;
+    const int kend = p0 + last_q + 1;
     const int ntiles = (kend + kFK - 1) / kFK;
     constexpr int CPR = DH / 8;  // 16-byte chunks per row
 
@@ -165,7 +167,7 @@ __global__ void __launch_bounds__(kFThreads) attn_prefill_tc_kernel(const __grid
 
     // this thread's two query rows: g and g + 8 of the warp's 16
     const int rq0 = warp * 16 + g, rq1 = rq0 + 8;
-    const int pos0 = a.p0 + min(q0 + rq0, a.T - 1), pos1 = a.p0 + min(q0 + rq1, a.T - 1);
+    const int pos0 = p0 + min(q0 + rq0, a.T - 1), pos1 = p0 + min(q0 + rq1, a.T - 1);
     const float sl2 = a.scale * 1.4426950408889634f;  // scores in log2 units
     float m0 = -CUDART_INF_F, m1 = -CUDART_INF_F, l0 = 0.f, l1 = 0.f;
     float o[DH / 8][4];

@@ -92,7 +92,7 @@ __global__ void __launch_bounds__(NT) gemm_simt_kernel(const __grid_constant__ G
             } else if (a.epi == kGemmAddF32) {
                 static_cast<float*>(a.y)[static_cast<long long>(t) * a.y_ld + sg.y_off + n] += v;
             } else {  // kGemmQKV
-                const int b = t / a.T, pos = a.p0 + t % a.T;
+                const int b = t / a.T, pos = (a.p0_dev ? *a.p0_dev : a.p0) + t % a.T;
                 float out = v;
                 if (sg.epi != kEpiV) {
                     const float other = acc[0][i][j ^ 1];

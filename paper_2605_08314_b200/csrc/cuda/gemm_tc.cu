@@ -20,6 +20,7 @@
 #include <cuda.h>
 
 #include <algorithm>
+#include <cstdlib>
 #include <stdexcept>
 #include <string>
 
@@ -47,7 +48,8 @@ struct TcArgs {
     CUtensorMap xmap;  // X [rows][x_ld] bf16, box 64 x 128, SWIZZLE_128B
     GemmArgs g;
     int seg_tiles[3];  // BN-wide output tiles per segment
-    int splits;        // split-K factor (blockIdx.z = split; > 1 only for kGemmStore)
+    int splits;        // split-K factor (blockIdx.z = split; > 1 only for kGemmStore / kGemmAddF32)
+    int dbg;           // development: bit 0 = skip the MMAs (operand-stream-only timing)
 };
 
 // ----------------------------------------------------------------- PTX ----
@@ -175,7 +177,8 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_tc_kernel(const __grid_const
     const GemvSeg& sg = g.seg[s];
     const int n0 = tile * BN, m0 = blockIdx.x * BM;
     constexpr int kAcc = DUAL ? 2 : 1;
-    constexpr uint32_t kCols = DUAL ? 2 * BN : BN;
+    constexpr uint32_t kAccStride = 256;  // dual: gate accumulator at TMEM column 256
+    constexpr uint32_t kCols = DUAL ? 2 * kAccStride : BN;
     constexpr uint32_t kAllocCols = kCols <= 32 ? 32 : kCols <= 64 ? 64 : kCols <= 128 ? 128 : kCols <= 256 ? 256 : 512;
 
     if (threadIdx.x == 0) {
@@ -239,7 +242,7 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_tc_kernel(const __grid_const
                 const int nk = seg_of(j).layout(2).nlines();
                 const int kb0 = nk * static_cast<int>(blockIdx.z) / A.splits;
                 const int kb1 = nk * (static_cast<int>(blockIdx.z) + 1) / A.splits;
-                const uint32_t tacc = tmem_base + static_cast<uint32_t>(j * BN);
+                const uint32_t tacc = tmem_base + static_cast<uint32_t>(j) * kAccStride;
 #pragma unroll 1
                 for (int kb = kb0; kb < kb1; ++kb, ++it) {
                     const int st = it % C::kStages;
@@ -249,9 +252,11 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_tc_kernel(const __grid_const
                     const uint32_t sa = smem_u32(smem + st * C::kStageBytes);
                     const uint32_t sb = sa + kABytes;
                     const uint64_t da = sw128_desc(sa), db = sw128_desc(sb);
+                    if (!(A.dbg & 1)) {
 #pragma unroll
-                    for (int k = 0; k < BK / 16; ++k)  // +32 B per K=16 step inside the 128 B swizzle atom
-                        tc_mma(tacc, da + 2 * k, db + 2 * k, idesc, (kb != kb0 || k != 0) ? 1u : 0u);
+                        for (int k = 0; k < BK / 16; ++k)  // +32 B per K=16 step inside the 128 B swizzle atom
+                            tc_mma(tacc, da + 2 * k, db + 2 * k, idesc, (kb != kb0 || k != 0) ? 1u : 0u);
+                    }
                     tc_commit(&empty[st]);
                 }
             }
@@ -269,7 +274,7 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_tc_kernel(const __grid_const
         for (int c0 = 0; c0 < BN; c0 += 32) {
             float v[32], gt[32];
             tmem_ld32(lane_addr + c0, v);  // .sync.aligned: every lane, before any divergence
-            if constexpr (DUAL) tmem_ld32(lane_addr + BN + c0, gt);
+            if constexpr (DUAL) tmem_ld32(lane_addr + kAccStride + c0, gt);
             const int n = n0 + c0;
             const int valid = min(32, sg.rows - n);
             if (t >= g.M || valid <= 0) continue;
@@ -278,7 +283,7 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_tc_kernel(const __grid_const
                 for (int i = 0; i < 32; ++i) v[i] = silu_mul(gt[i], v[i]);
                 store_bf16x32(static_cast<__nv_bfloat16*>(g.y) + static_cast<long long>(t) * g.y_ld + sg.y_off + n, v,
                               valid);
-            } else if (g.epi == kGemmStore && A.splits > 1) {  // fp32 partial of this K split
+            } else if (A.splits > 1) {  // fp32 partial of this K split (plain store / residual add)
                 float* w = g.ws + (static_cast<size_t>(blockIdx.z) * g.M + t) * g.y_ld + sg.y_off + n;
 #pragma unroll
                 for (int i = 0; i < 32; ++i)
@@ -292,7 +297,7 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_tc_kernel(const __grid_const
                 for (int i = 0; i < 32; ++i)
                     if (i < valid) y[i] += v[i];
             } else {  // kGemmQKV: RoPE (interleaved pairs, math.hpp:30-44) + q store / KV append
-                const int b = t / g.T, pos = g.p0 + t % g.T;
+                const int b = t / g.T, pos = (g.p0_dev ? *g.p0_dev : g.p0) + t % g.T;
                 if (sg.epi != kEpiV) {
                     const float2* cs = g.rope + static_cast<long long>(pos) * (g.d_head / 2);
 #pragma unroll
@@ -342,7 +347,8 @@ EncodeTiled encode_fn() {
     return fn;
 }
 
-// Split-K reduction: Y[t][y_off + n] = bf16(sum_z ws[z][t][y_off + n]) in split order.
+// Split-K reduction in split order: Y[t][y_off + n] = bf16(sum_z ws[z][t][y_off + n])
+// (plain store) or Yf32[t][y_off + n] += sum_z ws[z][...] (residual add).
 __global__ void splitk_reduce_kernel(const __grid_constant__ TcArgs A) {
     const GemmArgs& g = A.g;
     const int t = blockIdx.y;
@@ -352,7 +358,10 @@ __global__ void splitk_reduce_kernel(const __grid_constant__ TcArgs A) {
             const size_t c = static_cast<size_t>(t) * g.y_ld + sg.y_off + n;
             float acc = g.ws[c];
             for (int z = 1; z < A.splits; ++z) acc += g.ws[static_cast<size_t>(z) * g.M * g.y_ld + c];
-            static_cast<__nv_bfloat16*>(g.y)[c] = __float2bfloat16_rn(acc);
+            if (g.epi == kGemmAddF32)
+                static_cast<float*>(g.y)[c] += acc;
+            else
+                static_cast<__nv_bfloat16*>(g.y)[c] = __float2bfloat16_rn(acc);
         }
     }
 }
@@ -399,36 +408,58 @@ void gemm_tc(const GemmArgs& a, int x_rows, cudaStream_t s) {
         for (int i = 0; i < nseg; ++i) t += (a.seg[i].rows + bn - 1) / bn;
         return t;
     };
-    // 128 x 256 tiles (A tile reused over twice the outputs, half the CTAs) when
-    // they still cover the SMs; 128 x 128 otherwise
-    const bool wide = count_tiles(256) * mt >= 120;
-    const int BN = wide ? 256 : 128;
+    int nk_max = 0, nk_min = 1 << 30;
+    for (int i = 0; i < a.nseg; ++i) {
+        nk_max = std::max(nk_max, a.seg[i].layout(2).nlines());
+        nk_min = std::min(nk_min, a.seg[i].layout(2).nlines());
+    }
+    const bool can_split = !dual && (a.epi == kGemmStore || a.epi == kGemmAddF32) && a.ws;
+    // Tile width and split-K factor from a wave model: the operand stream is the
+    // cost (L2 -> SM, ~50 GB/s per SM measured), a CTA streams its k-blocks of
+    // 16 KiB X + BN x 128 B of W, CTAs run in waves of 148, a K split adds its
+    // fp32 partials' round trip and a reduction launch.
+    constexpr int kBNs[] = {128, 160, 192, 224, 256};
+    constexpr double kSmRate = 50e9, kHbm = 6.0e12, kLaunch = 3e-6;
+    int best_bn = 128, best_sp = 1;
+    double best = 1e30;
+    for (int bn : kBNs) {
+        const int tiles = count_tiles(bn);
+        const int max_sp = can_split ? (a.M <= BM ? std::max(1, nk_min / 2) : std::max(1, std::min(4, nk_min / 4))) : 1;
+        for (int sp = 1; sp <= max_sp; ++sp) {
+            if (sp > 1 && static_cast<size_t>(sp) * a.M * a.y_ld > a.ws_floats) break;
+            const long long ctas = static_cast<long long>(tiles) * mt * sp;
+            const double waves = static_cast<double>((ctas + 147) / 148);
+            const double kb = (dual ? 2.0 : 1.0) * nk_max / sp;
+            double t = waves * kb * (16384.0 + 128.0 * bn) / kSmRate;
+            if (sp > 1) t += 2.0 * sp * a.M * a.y_ld * 4.0 / kHbm + kLaunch;
+            if (t < best * 0.999) {
+                best = t;
+                best_bn = bn;
+                best_sp = sp;
+            }
+        }
+    }
+    if (const char* e = std::getenv("FSVD_GEMM_BN")) best_bn = std::atoi(e);
+    if (const char* e = std::getenv("FSVD_GEMM_SPLITS"); e && can_split) best_sp = std::max(1, std::atoi(e));
+    if (const char* e = std::getenv("FSVD_GEMM_DBG")) ta.dbg = std::atoi(e);
+    const int BN = best_bn;
     int tiles = 0;
     for (int i = 0; i < nseg; ++i) {
         ta.seg_tiles[i] = (a.seg[i].rows + BN - 1) / BN;
         tiles += ta.seg_tiles[i];
     }
-    // split K when the output tiles cannot fill the SMs (skinny rank-space
-    // projections at small token counts); deterministic fixed-order reduction
-    ta.splits = 1;
-    if (!dual && a.epi == kGemmStore && a.ws) {
-        int nk_min = 1 << 30;
-        for (int i = 0; i < a.nseg; ++i) nk_min = std::min(nk_min, a.seg[i].layout(2).nlines());
-        int sp = 148 / std::max(1, tiles * mt);
-        sp = std::min({sp, 4, nk_min / 4});
-        if (sp > 1 && static_cast<size_t>(sp) * a.M * a.y_ld <= a.ws_floats) ta.splits = sp;
+    ta.splits = best_sp;
+#define FSVD_TC_BN(N)                                  \
+    if (BN == N) {                                     \
+        if (dual)                                      \
+            launch<N, true>(ta, tiles, a.M, s);        \
+        else                                           \
+            launch<N, false>(ta, tiles, a.M, s);       \
+        return;                                        \
     }
-    if (wide) {
-        if (dual)
-            launch<256, true>(ta, tiles, a.M, s);
-        else
-            launch<256, false>(ta, tiles, a.M, s);
-    } else {
-        if (dual)
-            launch<128, true>(ta, tiles, a.M, s);
-        else
-            launch<128, false>(ta, tiles, a.M, s);
-    }
+    FSVD_TC_BN(128) FSVD_TC_BN(160) FSVD_TC_BN(192) FSVD_TC_BN(224) FSVD_TC_BN(256)
+#undef FSVD_TC_BN
+    throw std::runtime_error("gemm_tc: unsupported tile width " + std::to_string(BN));
 }
 
 }  // namespace fsvd::k

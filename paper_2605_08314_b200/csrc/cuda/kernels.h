@@ -48,6 +48,7 @@ struct AttnPrefillArgs {
     int out_ld;
     int batch, T, p0, n_heads, d_head;
     float scale;
+    const int* p0_dev;   // non-null: p0 = *p0_dev (graph-replayed batched decode)
 };
 void attn_prefill(WType wt, const AttnPrefillArgs& a, cudaStream_t s);
 
@@ -72,11 +73,12 @@ struct GemmArgs {
     // QKV epilogue
     const float2* rope;
     int p0, T, d_head, n_heads;
+    const int* p0_dev;   // non-null: p0 = *p0_dev (graph-replayed batched decode)
     void* kcache;
     void* vcache;
     long long cache_bstride, cache_hstride;
-    // split-K scratch for the plain-store epilogue (few output tiles): fp32
-    // [splits][M][y_ld]; null disables split-K
+    // split-K scratch for the plain-store / residual epilogues (few output
+    // tiles): fp32 [splits][M][y_ld]; null disables split-K
     float* ws;
     size_t ws_floats;
 };
@@ -96,6 +98,12 @@ void rmsnorm_rows(WType wt, const float* x, int x_ld, const float* gamma, float 
 // Copy rows {(b*T + T-1)} of x to xl[b] (last position of each sequence).
 void gather_last(const float* x, int x_ld, int batch, int T, int d, float* xl, int xl_ld, cudaStream_t s);
 void set_int(int* p, int v, cudaStream_t s);
+// Greedy argmax of each logits row (ties -> lowest index, math.hpp:132-140):
+// tokens[b] = argmax(logits[b][0..V)); out[b][*step] = tokens[b] if out.
+void argmax_rows(const float* logits, int V, int batch, int* tokens, int* out, int out_ld, const int* step,
+                 cudaStream_t s);
+// *pos += pos_inc; *step += 1 (if step) -- after argmax_rows
+void advance_pos(int* pos, int pos_inc, int* step, cudaStream_t s);
 
 // Synthetic-weight generation (include/fsvd/synth.hpp stream). Logical tensor
 // element i = (r, c) of a rows x cols tensor goes to

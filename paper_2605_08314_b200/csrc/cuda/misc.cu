@@ -1,6 +1,8 @@
 // Small kernels around the prefill chain and model setup: embedding gather,
 // row RMSNorm (prefill prologue), last-position gather, the length-register
 // setter and the synthetic-weight generator.
+#include <math_constants.h>
+
 #include "common.cuh"
 #include "kernels.h"
 
@@ -98,6 +100,53 @@ __global__ void gather_last_kernel(const float* x, int x_ld, int T, int d, float
 }
 
 __global__ void set_int_kernel(int* p, int v) { *p = v; }
+
+// one CTA per row; ties -> lowest index (math.hpp:132-140)
+__global__ void __launch_bounds__(256) argmax_rows_kernel(const float* logits, int V, int* tokens, int* out, int out_ld,
+                                                          const int* step) {
+    __shared__ float sv[8];
+    __shared__ int si[8];
+    const int b = blockIdx.x;
+    const float* row = logits + static_cast<long long>(b) * V;
+    float bv = -CUDART_INF_F;
+    int bi = 0x7fffffff;
+    for (int i = threadIdx.x; i < V; i += 256) {
+        const float v = row[i];
+        if (v > bv) {  // strictly greater: the first (lowest) index wins within a thread
+            bv = v;
+            bi = i;
+        }
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+        const float ov = __shfl_xor_sync(0xffffffffu, bv, o);
+        const int oi = __shfl_xor_sync(0xffffffffu, bi, o);
+        if (ov > bv || (ov == bv && oi < bi)) {
+            bv = ov;
+            bi = oi;
+        }
+    }
+    if ((threadIdx.x & 31) == 0) {
+        sv[threadIdx.x >> 5] = bv;
+        si[threadIdx.x >> 5] = bi;
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        for (int w = 1; w < 8; ++w)
+            if (sv[w] > bv || (sv[w] == bv && si[w] < bi)) {
+                bv = sv[w];
+                bi = si[w];
+            }
+        if (bi == 0x7fffffff) bi = 0;
+        tokens[b] = bi;
+        if (out) out[static_cast<long long>(b) * out_ld + (step ? *step : 0)] = bi;
+    }
+}
+
+__global__ void advance_pos_kernel(int* pos, int inc, int* step) {
+    *pos += inc;
+    if (step) *step += 1;
+}
 
 __device__ __forceinline__ float round_bf16_dev(float x) {
     uint32_t u = __float_as_uint(x);
@@ -202,6 +251,13 @@ void gather_last(const float* x, int x_ld, int batch, int T, int d, float* xl, i
 }
 
 void set_int(int* p, int v, cudaStream_t s) { set_int_kernel<<<1, 1, 0, s>>>(p, v); }
+
+void argmax_rows(const float* logits, int V, int batch, int* tokens, int* out, int out_ld, const int* step,
+                 cudaStream_t s) {
+    argmax_rows_kernel<<<batch, 256, 0, s>>>(logits, V, tokens, out, out_ld, step);
+}
+
+void advance_pos(int* pos, int pos_inc, int* step, cudaStream_t s) { advance_pos_kernel<<<1, 1, 0, s>>>(pos, pos_inc, step); }
 
 void synth_fill(const SynthFill& f, cudaStream_t s) {
     const long long n = f.rows * f.cols;

@@ -396,8 +396,12 @@ Session::Session(DeviceModel* m, const fsvd_session_opts& o) : m_(m) {
     const ModelConfig& c = m->cfg;
     B_ = static_cast<int>(o.batch);
     if (B_ < 1) throw ConfigError("session batch must be >= 1");
-    if (B_ > 2) throw ConfigError("decode batch > 2 is not supported by the decode megakernel yet");
-    if (m_->cfg.d_model > 8192) throw ConfigError("d_model > 8192 is not supported by the decode megakernel");
+    // B <= 2: the persistent decode megakernel; larger batches: the batched
+    // layer engine (FSVD_BATCHED=1 forces it for any batch)
+    batched_ = B_ > 2;
+    if (const char* e = std::getenv("FSVD_BATCHED"); e && e[0] == '1') batched_ = true;
+    if (!batched_ && m_->cfg.d_model > 8192)
+        throw ConfigError("d_model > 8192 is not supported by the decode megakernel");
     if (!(c.d_head == 32 || c.d_head == 64 || c.d_head == 128))
         throw ConfigError("d_head must be 32, 64 or 128 for the sm_100a kernels");
     cap_ = o.capacity ? o.capacity : (m->capacity ? m->capacity : 8192);
@@ -451,9 +455,13 @@ Session::Session(DeviceModel* m, const fsvd_session_opts& o) : m_(m) {
         mk_grid_ = std::min(mk_grid_, std::atoi(g));
     mk_grid_ = std::min(mk_grid_, 256);  // attention merge scratch is sized for <= 256 pieces per head
     mk_splits_ = mk_grid_;  // attention partial slots per head: one per contributing CTA
-    attn_part_ = static_cast<float*>(dalloc(4ull * B_ * H * mk_splits_ * (dh + 2)));
-    attn_count_ = static_cast<unsigned*>(dalloc(4ull * B_ * H));
-    build_program();
+    if (batched_) {
+        ensure_prefill_workspace(B_);
+    } else {
+        attn_part_ = static_cast<float*>(dalloc(4ull * B_ * H * mk_splits_ * (dh + 2)));
+        attn_count_ = static_cast<unsigned*>(dalloc(4ull * B_ * H));
+        build_program();
+    }
     FSVD_CUDA(cudaStreamSynchronize(stream_));
     stats_.allocs = 0;
 }
@@ -463,6 +471,7 @@ Session::~Session() {
     if (stream_) cudaStreamSynchronize(stream_);
     for (auto g : layer_graphs_) cudaGraphExecDestroy(g);
     if (step_graph_) cudaGraphExecDestroy(step_graph_);
+    if (bstep_graph_) cudaGraphExecDestroy(bstep_graph_);
     for (void* p : allocations_) cudaFree(p);
     if (stream_) cudaStreamDestroy(stream_);
 }
@@ -838,7 +847,7 @@ void Session::decode_step(const int32_t* d_tokens, float* d_logits) {
     if (position_ >= cap_) throw CapacityError("decode_step: KV cache full (capacity " + std::to_string(cap_) + ")");
     if (d_tokens) FSVD_CUDA(cudaMemcpyAsync(tokens_, d_tokens, 4ull * B_, cudaMemcpyDeviceToDevice, stream_));
     const uint64_t before = stats_.dispatches;
-    mk_decode(nullptr, 0);
+    decode_any(nullptr, 0);
     if (d_logits && d_logits != logits_)
         FSVD_CUDA(cudaMemcpyAsync(d_logits, logits_, 4ull * B_ * m_->cfg.vocab, cudaMemcpyDeviceToDevice, stream_));
     FSVD_CUDA(cudaGetLastError());
@@ -863,7 +872,9 @@ void Session::ensure_prefill_workspace(size_t rows) {
     pf_pd_ = dalloc(rows * ld_d_ * es);
     pf_tok_ = static_cast<int32_t*>(dalloc(rows * 4));
     // split-K scratch (only used while rows <= 1024: few output tiles)
-    pf_ws_floats_ = 4ull * std::min<size_t>(rows, 1024) * std::max({ld_qkv_, ld_o_, ld_ug_, ld_d_});
+    // (decode-sized M: up to 64 splits per projection, residual adds included)
+    pf_ws_floats_ = std::max(4ull * std::min<size_t>(rows, 1024), 64ull * std::min<size_t>(rows, 64)) *
+                    std::max({ld_qkv_, ld_o_, ld_ug_, ld_d_, m.ldd});
     pf_ws_ = m.wt == k::kBF16 ? static_cast<float*>(dalloc(4 * pf_ws_floats_)) : nullptr;
     pf_rows_ = rows;
     stats_.allocs += 11;
@@ -874,13 +885,19 @@ void Session::prefill_chunk(const int32_t* d_tokens, size_t T_total, size_t t0, 
     const DeviceModel& m = *m_;
     const ModelConfig& c = m.cfg;
     const int M = static_cast<int>(B_ * Tc);
-    const int d = static_cast<int>(c.d_model), ldd = m.ldd, ldff = m.ldff;
-    const float eps = static_cast<float>(c.norm_eps);
-    const size_t es = m.esize;
+    const int d = static_cast<int>(c.d_model), ldd = m.ldd;
     FSVD_CUDA(cudaMemcpy2DAsync(pf_tok_, Tc * 4, d_tokens + t0, T_total * 4, Tc * 4, B_, cudaMemcpyDeviceToDevice,
                                 stream_));
     k::embed(m.wt, m.emb, ldd, pf_tok_, M, d, pf_x_, ldd, stream_);
-    const int p0 = static_cast<int>(position_);
+    layers_forward(M, static_cast<int>(Tc), static_cast<int>(position_), nullptr);
+}
+
+void Session::layers_forward(int M, int Tc, int p0, const int* p0_dev) {
+    const DeviceModel& m = *m_;
+    const ModelConfig& c = m.cfg;
+    const int d = static_cast<int>(c.d_model), ldd = m.ldd, ldff = m.ldff;
+    const float eps = static_cast<float>(c.norm_eps);
+    const size_t es = m.esize;
     auto gemm = [&](const void* x, int x_ld, int nseg, std::initializer_list<k::GemvSeg> segs, int epi, void* y,
                     int y_ld, char* kc = nullptr, char* vc = nullptr) {
         k::GemmArgs g{};
@@ -895,7 +912,8 @@ void Session::prefill_chunk(const int32_t* d_tokens, size_t T_total, size_t t0, 
         g.y_ld = y_ld;
         g.rope = rope_;
         g.p0 = p0;
-        g.T = static_cast<int>(Tc);
+        g.p0_dev = p0_dev;
+        g.T = Tc;
         g.d_head = static_cast<int>(c.d_head);
         g.n_heads = static_cast<int>(c.n_heads);
         g.kcache = kc;
@@ -933,8 +951,9 @@ void Session::prefill_chunk(const int32_t* d_tokens, size_t T_total, size_t t0, 
             a.out = pf_att_;
             a.out_ld = ldd;
             a.batch = B_;
-            a.T = static_cast<int>(Tc);
+            a.T = Tc;
             a.p0 = p0;
+            a.p0_dev = p0_dev;
             a.n_heads = static_cast<int>(c.n_heads);
             a.d_head = static_cast<int>(c.d_head);
             a.scale = static_cast<float>(1.0 / std::sqrt(static_cast<double>(c.d_head)));
@@ -955,6 +974,72 @@ void Session::prefill_chunk(const int32_t* d_tokens, size_t T_total, size_t t0, 
         gemm(pf_h_, ldff, 1, {seg(L.at[kDown], 0, 0, k::kEpiStore)}, k::kGemmStore, pf_pd_, ld_d_);
         gemm(pf_pd_, ld_d_, 1, {seg(L.bt[kDown], 0, 0, k::kEpiStore)}, k::kGemmAddF32, pf_x_, ldd);
     }
+}
+
+// Batched engine head: logits[b] = RMSNorm(x[b]) . head (fp32, zeroed then
+// accumulated by the head GEMM's residual-add epilogue), greedy argmax into
+// tokens_ (and d_out[b][*step]), then pos += pos_inc, step += 1 -- the same
+// contract as the megakernel's head + argmax phases.
+void Session::head_rows(const float* x, int32_t* d_out, int out_ld, int pos_inc) {
+    const DeviceModel& m = *m_;
+    const ModelConfig& c = m.cfg;
+    const int V = static_cast<int>(c.vocab);
+    k::rmsnorm_rows(m.wt, x, m.ldd, m.final_gamma, static_cast<float>(c.norm_eps), B_, static_cast<int>(c.d_model),
+                    pf_xn_, m.ldd, stream_);
+    FSVD_CUDA(cudaMemsetAsync(logits_, 0, 4ull * B_ * V, stream_));
+    k::GemmArgs g{};
+    g.x = pf_xn_;
+    g.x_ld = m.ldd;
+    g.M = B_;
+    g.seg[0] = seg(m.head_t, 0, 0, k::kEpiStore);
+    g.nseg = 1;
+    g.epi = k::kGemmAddF32;
+    g.y = logits_;
+    g.y_ld = V;
+    g.ws = pf_ws_;
+    g.ws_floats = pf_ws_floats_;
+    k::gemm(m.wt, g, stream_);
+    k::argmax_rows(logits_, V, B_, tokens_, d_out, out_ld, step_, stream_);
+    k::advance_pos(pos_, pos_inc, step_, stream_);
+    launches_this_step_ += 5;
+}
+
+// One batched decode step: embed tokens_ -> every layer at M = B rows, T = 1,
+// positions read from the device length register -> head + argmax. Eager
+// plan: direct launches; graph plans: the step is captured once (per output
+// buffer) and replayed.
+void Session::batched_decode(int32_t* d_out, int out_ld) {
+    const DeviceModel& m = *m_;
+    auto body = [&] {
+        k::embed(m.wt, m.emb, m.ldd, tokens_, B_, static_cast<int>(m.cfg.d_model), pf_x_, m.ldd, stream_);
+        layers_forward(B_, 1, 0, pos_);
+        head_rows(pf_x_, d_out, out_ld, 1);
+    };
+    launches_this_step_ = 0;
+    if (plan_ == FSVD_PLAN_EAGER) {
+        body();
+        const uint64_t n = launches_this_step_ + 1 + 10ull * m.cfg.n_layers;
+        stats_.dispatches += n;
+        stats_.kernel_launches += n;
+        return;
+    }
+    if (bstep_graph_ && (d_out != bstep_out_ || out_ld != bstep_out_ld_)) {
+        FSVD_CUDA(cudaGraphExecDestroy(bstep_graph_));
+        bstep_graph_ = nullptr;
+    }
+    if (!bstep_graph_) {
+        cudaGraph_t g;
+        FSVD_CUDA(cudaStreamBeginCapture(stream_, cudaStreamCaptureModeThreadLocal));
+        body();
+        FSVD_CUDA(cudaStreamEndCapture(stream_, &g));
+        FSVD_CUDA(cudaGraphInstantiate(&bstep_graph_, g, 0));
+        cudaGraphDestroy(g);
+        bstep_out_ = d_out;
+        bstep_out_ld_ = out_ld;
+    }
+    FSVD_CUDA(cudaGraphLaunch(bstep_graph_, stream_));
+    stats_.graph_launches += 1;
+    stats_.dispatches += 1;
 }
 
 void Session::prefill(const int32_t* d_tokens, size_t T, float* d_logits) {
@@ -980,7 +1065,10 @@ void Session::prefill(const int32_t* d_tokens, size_t T, float* d_logits) {
     // first generated token (pos_inc = 0: pos already advanced)
     k::set_int(step_, 0, stream_);
     launches_this_step_ = 0;
-    mk_run(ph_pf_head_, ph_pf_argmax_ + 1);
+    if (batched_)
+        head_rows(x_, nullptr, 0, 0);
+    else
+        mk_run(ph_pf_head_, ph_pf_argmax_ + 1);
     if (d_logits && d_logits != logits_)
         FSVD_CUDA(cudaMemcpyAsync(d_logits, logits_, 4ull * B_ * c.vocab, cudaMemcpyDeviceToDevice, stream_));
     FSVD_CUDA(cudaGetLastError());
@@ -997,7 +1085,7 @@ void Session::generate(const int32_t* d_prompt, size_t T, size_t max_new, int32_
     k::set_int(step_, 1, stream_);
     for (size_t i = 1; i < max_new; ++i) {
         const uint64_t before = stats_.dispatches;
-        mk_decode(d_out, static_cast<int>(max_new));
+        decode_any(d_out, static_cast<int>(max_new));
         stats_.last_dispatches = stats_.dispatches - before;
         stats_.steps += 1;
         position_ += 1;

@@ -110,7 +110,11 @@ class Session {
     void* staging(size_t bytes);
     // copies the last traced full step: [grid][phases][4] ns stamps; returns phases
     int read_trace(unsigned long long* out, size_t count, int* grid);
-    std::array<int, 4> engine() const { return {1, k::kChunkBytes, mk_stages_, mk_splits_}; }
+    // {1 megakernel | 2 batched layer engine, ring chunk bytes, ring stages, attention splits}
+    std::array<int, 4> engine() const {
+        return batched_ ? std::array<int, 4>{2, 0, 0, 0} : std::array<int, 4>{1, k::kChunkBytes, mk_stages_, mk_splits_};
+    }
+    bool batched() const { return batched_; }
 
   private:
     void build_program();
@@ -119,6 +123,12 @@ class Session {
     void mk_decode(int32_t* d_out, int out_ld);
     void mk_set_out(int32_t* d_out, int out_ld);
     void prefill_chunk(const int32_t* d_tokens, size_t T_total, size_t t0, size_t Tc);
+    // every layer over M = B*T rows of pf_x_ (positions p0 + t, or *p0_dev + t)
+    void layers_forward(int M, int T, int p0, const int* p0_dev);
+    // batched engine (B > 2): final norm + head GEMM + argmax over rows x[B]
+    void head_rows(const float* x, int32_t* d_out, int out_ld, int pos_inc);
+    void batched_decode(int32_t* d_out, int out_ld);
+    void decode_any(int32_t* d_out, int out_ld) { batched_ ? batched_decode(d_out, out_ld) : mk_decode(d_out, out_ld); }
     void ensure_prefill_workspace(size_t rows);
     void* dalloc(size_t bytes);
     k::GemvSeg seg(const DeviceMatrix& m, int x_off, int y_off, int epi) const;
@@ -175,6 +185,13 @@ class Session {
     int32_t* mk_out_ = nullptr;
     int mk_out_ld_ = 0;
     uint64_t launches_this_step_ = 0;
+
+    // batched engine (B > 2, or FSVD_BATCHED=1): layer-by-layer tcgen05 GEMMs
+    // with the batch as the M dimension, one graph per step for the graph plans
+    bool batched_ = false;
+    cudaGraphExec_t bstep_graph_ = nullptr;
+    int32_t* bstep_out_ = nullptr;
+    int bstep_out_ld_ = 0;
 
     // plans
     std::vector<cudaGraphExec_t> layer_graphs_;
