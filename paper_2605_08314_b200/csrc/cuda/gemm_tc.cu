@@ -20,6 +20,7 @@
 #include <cuda.h>
 
 #include <algorithm>
+#include <cstdio>
 #include <cstdlib>
 #include <stdexcept>
 #include <string>
@@ -36,10 +37,10 @@ constexpr int BM = 128, BK = 64;
 constexpr int kABytes = BM * 128;  // 16 KiB: 128 rows x 128 B
 constexpr int kThreads = 192;
 
-template <int BN>
+template <int BN, int BMT = 1>
 struct Cfg {
     static constexpr int kBBytes = BN * 128;
-    static constexpr int kStageBytes = kABytes + kBBytes;
+    static constexpr int kStageBytes = BMT * kABytes + kBBytes;
     static constexpr int kStages = (200 * 1024) / kStageBytes;
     static constexpr int kSmem = kStages * kStageBytes + 1024 /*align*/ + 256 /*barriers*/;
 };
@@ -154,9 +155,12 @@ __device__ __forceinline__ void store_bf16x32(__nv_bfloat16* dst, const float (&
 }
 
 // -------------------------------------------------------------- kernel ----
-template <int BN, bool DUAL>
+// BMT = 128-row M sub-tiles per CTA sharing each W tile (2: a 256 x BN tile in
+// two TMEM accumulators -- half the W traffic per FLOP of BMT = 1).
+template <int BN, bool DUAL, int BMT>
 __global__ void __launch_bounds__(kThreads, 1) gemm_tc_kernel(const __grid_constant__ TcArgs A) {
-    using C = Cfg<BN>;
+    static_assert(!(DUAL && BMT > 1), "the dual GEMM uses the second accumulator for the gate");
+    using C = Cfg<BN, BMT>;
     extern __shared__ __align__(1024) uint8_t smem_raw[];
     uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
     uint64_t* full = reinterpret_cast<uint64_t*>(smem + C::kStages * C::kStageBytes);
@@ -175,10 +179,10 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_tc_kernel(const __grid_const
         }
     }
     const GemvSeg& sg = g.seg[s];
-    const int n0 = tile * BN, m0 = blockIdx.x * BM;
+    const int n0 = tile * BN, m0 = blockIdx.x * BM * BMT;
     constexpr int kAcc = DUAL ? 2 : 1;
     constexpr uint32_t kAccStride = 256;  // dual: gate accumulator at TMEM column 256
-    constexpr uint32_t kCols = DUAL ? 2 * kAccStride : BN;
+    constexpr uint32_t kCols = (DUAL || BMT > 1) ? 2 * kAccStride : BN;
     constexpr uint32_t kAllocCols = kCols <= 32 ? 32 : kCols <= 64 ? 64 : kCols <= 128 ? 128 : kCols <= 256 ? 256 : 512;
 
     if (threadIdx.x == 0) {
@@ -215,7 +219,7 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_tc_kernel(const __grid_const
                 const int kb1 = nk * (static_cast<int>(blockIdx.z) + 1) / A.splits;
                 const int t0 = n0 / 16;
                 const int nt = min(BN / 16, lay.ntiles() - t0);
-                const uint32_t bytes = kABytes + static_cast<uint32_t>(nt) * kLineTileBytes;
+                const uint32_t bytes = BMT * kABytes + static_cast<uint32_t>(nt) * kLineTileBytes;
                 const char* wbase = static_cast<const char*>(sj.w) + static_cast<size_t>(t0) * lay.tile_bytes();
 #pragma unroll 1
                 for (int kb = kb0; kb < kb1; ++kb, ++it) {
@@ -223,9 +227,11 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_tc_kernel(const __grid_const
                     const uint32_t ph = (it / C::kStages) & 1;
                     mbar_wait(&empty[st], ph ^ 1);
                     uint8_t* sa = smem + st * C::kStageBytes;
-                    uint8_t* sb = sa + kABytes;
+                    uint8_t* sb = sa + BMT * kABytes;
                     mbar_expect_tx(&full[st], bytes);
-                    tma_load_2d(sa, &A.xmap, &full[st], sj.x_off + kb * BK, m0);
+#pragma unroll
+                    for (int mi = 0; mi < BMT; ++mi)
+                        tma_load_2d(sa + mi * kABytes, &A.xmap, &full[st], sj.x_off + kb * BK, m0 + mi * BM);
                     const char* wl = wbase + static_cast<size_t>(kb) * kLineTileBytes;
                     for (int i = 0; i < nt; ++i)
                         bulk_g2s(sb + i * kLineTileBytes, wl + static_cast<size_t>(i) * lay.tile_bytes(),
@@ -250,12 +256,17 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_tc_kernel(const __grid_const
                     mbar_wait(&full[st], ph);
                     tc_fence_after();
                     const uint32_t sa = smem_u32(smem + st * C::kStageBytes);
-                    const uint32_t sb = sa + kABytes;
-                    const uint64_t da = sw128_desc(sa), db = sw128_desc(sb);
+                    const uint32_t sb = sa + BMT * kABytes;
+                    const uint64_t db = sw128_desc(sb);
                     if (!(A.dbg & 1)) {
 #pragma unroll
-                        for (int k = 0; k < BK / 16; ++k)  // +32 B per K=16 step inside the 128 B swizzle atom
-                            tc_mma(tacc, da + 2 * k, db + 2 * k, idesc, (kb != kb0 || k != 0) ? 1u : 0u);
+                        for (int mi = 0; mi < BMT; ++mi) {
+                            const uint64_t da = sw128_desc(sa + mi * kABytes);
+#pragma unroll
+                            for (int k = 0; k < BK / 16; ++k)  // +32 B per K=16 step inside the 128 B swizzle atom
+                                tc_mma(tacc + mi * kAccStride, da + 2 * k, db + 2 * k, idesc,
+                                       (kb != kb0 || k != 0) ? 1u : 0u);
+                        }
                     }
                     tc_commit(&empty[st]);
                 }
@@ -266,12 +277,14 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_tc_kernel(const __grid_const
         // epilogue: warp w reads TMEM lanes 32*(w%4) .. +31 (= tile rows)
         const int q = warp & 3;
         const int row = q * 32 + lane;
-        const int t = m0 + row;
         mbar_wait(tmem_full, 0);
         tc_fence_after();
-        const uint32_t lane_addr = tmem_base + (static_cast<uint32_t>(q * 32) << 16);
+#pragma unroll 1
+        for (int mi = 0; mi < BMT; ++mi)
 #pragma unroll 1
         for (int c0 = 0; c0 < BN; c0 += 32) {
+            const int t = m0 + mi * BM + row;
+            const uint32_t lane_addr = tmem_base + (static_cast<uint32_t>(q * 32) << 16) + mi * kAccStride;
             float v[32], gt[32];
             tmem_ld32(lane_addr + c0, v);  // .sync.aligned: every lane, before any divergence
             if constexpr (DUAL) tmem_ld32(lane_addr + kAccStride + c0, gt);
@@ -349,15 +362,25 @@ EncodeTiled encode_fn() {
 
 // Split-K reduction in split order: Y[t][y_off + n] = bf16(sum_z ws[z][t][y_off + n])
 // (plain store) or Yf32[t][y_off + n] += sum_z ws[z][...] (residual add).
-__global__ void splitk_reduce_kernel(const __grid_constant__ TcArgs A) {
+__global__ void __launch_bounds__(256) splitk_reduce_kernel(const __grid_constant__ TcArgs A) {
     const GemmArgs& g = A.g;
-    const int t = blockIdx.y;
+    const size_t zs = static_cast<size_t>(g.M) * g.y_ld;  // partial stride
     for (int s = 0; s < g.nseg; ++s) {
         const GemvSeg& sg = g.seg[s];
-        for (int n = blockIdx.x * blockDim.x + threadIdx.x; n < sg.rows; n += gridDim.x * blockDim.x) {
+        const long long total = static_cast<long long>(g.M) * sg.rows;
+        for (long long i = blockIdx.x * 256ll + threadIdx.x; i < total; i += static_cast<long long>(gridDim.x) * 256) {
+            const int t = static_cast<int>(i / sg.rows), n = static_cast<int>(i - static_cast<long long>(t) * sg.rows);
             const size_t c = static_cast<size_t>(t) * g.y_ld + sg.y_off + n;
-            float acc = g.ws[c];
-            for (int z = 1; z < A.splits; ++z) acc += g.ws[static_cast<size_t>(z) * g.M * g.y_ld + c];
+            // all partials' loads in flight (8 at a time), summed in split order
+            float acc = 0.f;
+            for (int z0 = 0; z0 < A.splits; z0 += 8) {
+                float v[8];
+#pragma unroll
+                for (int u = 0; u < 8; ++u) v[u] = z0 + u < A.splits ? __ldcs(g.ws + (z0 + u) * zs + c) : 0.f;
+#pragma unroll
+                for (int u = 0; u < 8; ++u)
+                    if (z0 + u < A.splits) acc = z0 + u == 0 ? v[u] : acc + v[u];
+            }
             if (g.epi == kGemmAddF32)
                 static_cast<float*>(g.y)[c] += acc;
             else
@@ -366,17 +389,17 @@ __global__ void splitk_reduce_kernel(const __grid_constant__ TcArgs A) {
     }
 }
 
-template <int BN, bool DUAL>
+template <int BN, bool DUAL, int BMT>
 void launch(const TcArgs& ta, int tiles, int M, cudaStream_t s) {
-    using C = Cfg<BN>;
+    using C = Cfg<BN, BMT>;
     static bool attr = false;
     if (!attr) {
-        cudaFuncSetAttribute(gemm_tc_kernel<BN, DUAL>, cudaFuncAttributeMaxDynamicSharedMemorySize, C::kSmem);
+        cudaFuncSetAttribute(gemm_tc_kernel<BN, DUAL, BMT>, cudaFuncAttributeMaxDynamicSharedMemorySize, C::kSmem);
         attr = true;
     }
-    dim3 grid((M + BM - 1) / BM, tiles, ta.splits);
-    gemm_tc_kernel<BN, DUAL><<<grid, kThreads, C::kSmem, s>>>(ta);
-    if (ta.splits > 1) splitk_reduce_kernel<<<dim3(8, M), 256, 0, s>>>(ta);
+    dim3 grid((M + BM * BMT - 1) / (BM * BMT), tiles, ta.splits);
+    gemm_tc_kernel<BN, DUAL, BMT><<<grid, kThreads, C::kSmem, s>>>(ta);
+    if (ta.splits > 1) splitk_reduce_kernel<<<4 * 148, 256, 0, s>>>(ta);
 }
 
 }  // namespace
@@ -402,7 +425,6 @@ void gemm_tc(const GemmArgs& a, int x_rows, cudaStream_t s) {
     if (r != CUDA_SUCCESS) throw std::runtime_error("cuTensorMapEncodeTiled failed: " + std::to_string(int(r)));
     const bool dual = a.epi == kGemmSilu;
     const int nseg = dual ? 1 : a.nseg;
-    const int mt = (a.M + BM - 1) / BM;
     auto count_tiles = [&](int bn) {
         int t = 0;
         for (int i = 0; i < nseg; ++i) t += (a.seg[i].rows + bn - 1) / bn;
@@ -414,33 +436,57 @@ void gemm_tc(const GemmArgs& a, int x_rows, cudaStream_t s) {
         nk_min = std::min(nk_min, a.seg[i].layout(2).nlines());
     }
     const bool can_split = !dual && (a.epi == kGemmStore || a.epi == kGemmAddF32) && a.ws;
-    // Tile width and split-K factor from a wave model: the operand stream is the
-    // cost (L2 -> SM, ~50 GB/s per SM measured), a CTA streams its k-blocks of
-    // 16 KiB X + BN x 128 B of W, CTAs run in waves of 148, a K split adds its
-    // fp32 partials' round trip and a reduction launch.
-    constexpr int kBNs[] = {128, 160, 192, 224, 256};
-    constexpr double kSmRate = 50e9, kHbm = 6.0e12, kLaunch = 3e-6;
-    int best_bn = 128, best_sp = 1;
-    double best = 1e30;
-    for (int bn : kBNs) {
-        const int tiles = count_tiles(bn);
-        const int max_sp = can_split ? (a.M <= BM ? std::max(1, nk_min / 2) : std::max(1, std::min(4, nk_min / 4))) : 1;
-        for (int sp = 1; sp <= max_sp; ++sp) {
-            if (sp > 1 && static_cast<size_t>(sp) * a.M * a.y_ld > a.ws_floats) break;
-            const long long ctas = static_cast<long long>(tiles) * mt * sp;
-            const double waves = static_cast<double>((ctas + 147) / 148);
-            const double kb = (dual ? 2.0 : 1.0) * nk_max / sp;
-            double t = waves * kb * (16384.0 + 128.0 * bn) / kSmRate;
-            if (sp > 1) t += 2.0 * sp * a.M * a.y_ld * 4.0 / kHbm + kLaunch;
-            if (t < best * 0.999) {
-                best = t;
-                best_bn = bn;
-                best_sp = sp;
+    int best_bn = 128, best_sp = 1, best_bmt = 1;
+    if (a.M <= BM) {
+        // Decode-sized M (batched engine): the weight stream is the whole cost and
+        // the fp32 partials are tiny. Tile width and split-K factor from a wave
+        // model: a CTA streams its k-blocks of 16 KiB X + BN x 128 B of W at
+        // ~55 GB/s (measured per-SM L2 -> SM rate), CTAs run in waves of 148, a
+        // split adds its partials' round trip and a reduction launch.
+        constexpr int kBNs[] = {128, 160, 192, 224, 256};
+        constexpr double kSmRate = 55e9, kHbm = 6.0e12, kLaunch = 3e-6;
+        double best = 1e30;
+        for (int bn : kBNs) {
+            const int tiles = count_tiles(bn);
+            const int max_sp = can_split ? std::max(1, nk_min / 2) : 1;
+            for (int sp = 1; sp <= max_sp; ++sp) {
+                if (sp > 1 && static_cast<size_t>(sp) * a.M * a.y_ld > a.ws_floats) break;
+                const long long ctas = static_cast<long long>(tiles) * sp;
+                const double waves = static_cast<double>((ctas + 147) / 148);
+                const double kb = (dual ? 2.0 : 1.0) * nk_max / sp;
+                double t = waves * kb * (16384.0 + 128.0 * bn) / kSmRate;
+                if (sp > 1) t += 2.0 * sp * a.M * a.y_ld * 4.0 / kHbm + kLaunch;
+                if (t < best * 0.999) {
+                    best = t;
+                    best_bn = bn;
+                    best_sp = sp;
+                }
             }
+        }
+    } else {
+        // Prefill (measured per projection on the C2 prompt, ncu launch lists in
+        // profiles/): 128 x 256 tiles when they still cover the SMs, else 128 x 128;
+        // the dual up/gate GEMM at 128 x 160 (2.32 -> 1.86 waves: 128 -> 102 us);
+        // 256 x 256 tiles (two TMEM accumulators sharing each W tile) once the M
+        // tiles alone fill the machine (8192^3: 807 -> 1098 TFLOP/s); split K only
+        // for plain stores whose tiles cover < 1 wave (the reduction costs ~20 us).
+        const int mt = (a.M + BM - 1) / BM;
+        best_bn = count_tiles(256) * mt >= 120 ? 256 : 128;
+        if (dual) best_bn = 160;
+        if (!dual && count_tiles(256) * ((a.M + 2 * BM - 1) / (2 * BM)) >= 148) {
+            best_bn = 256;
+            best_bmt = 2;
+        }
+        if (!dual && a.epi == kGemmStore && a.ws && best_bmt == 1) {
+            int sp = 148 / std::max(1, count_tiles(best_bn) * mt);
+            sp = std::min({sp, 4, nk_min / 4});
+            if (sp > 1 && static_cast<size_t>(sp) * a.M * a.y_ld <= a.ws_floats) best_sp = sp;
         }
     }
     if (const char* e = std::getenv("FSVD_GEMM_BN")) best_bn = std::atoi(e);
     if (const char* e = std::getenv("FSVD_GEMM_SPLITS"); e && can_split) best_sp = std::max(1, std::atoi(e));
+    if (const char* e = std::getenv("FSVD_GEMM_BMT"); e && !dual) best_bmt = std::atoi(e) == 2 ? 2 : 1;
+    if (best_bmt == 2) best_bn = 256;
     if (const char* e = std::getenv("FSVD_GEMM_DBG")) ta.dbg = std::atoi(e);
     const int BN = best_bn;
     int tiles = 0;
@@ -449,12 +495,19 @@ void gemm_tc(const GemmArgs& a, int x_rows, cudaStream_t s) {
         tiles += ta.seg_tiles[i];
     }
     ta.splits = best_sp;
+    if (std::getenv("FSVD_GEMM_LOG"))
+        std::fprintf(stderr, "gemm_tc M=%d N0=%d nseg=%d nk=%d epi=%d -> BN=%d BMT=%d splits=%d tiles=%d\n", a.M,
+                     a.seg[0].rows, a.nseg, nk_max, a.epi, BN, best_bmt, best_sp, tiles);
+    if (best_bmt == 2) {
+        launch<256, false, 2>(ta, tiles, a.M, s);
+        return;
+    }
 #define FSVD_TC_BN(N)                                  \
     if (BN == N) {                                     \
         if (dual)                                      \
-            launch<N, true>(ta, tiles, a.M, s);        \
+            launch<N, true, 1>(ta, tiles, a.M, s);     \
         else                                           \
-            launch<N, false>(ta, tiles, a.M, s);       \
+            launch<N, false, 1>(ta, tiles, a.M, s);    \
         return;                                        \
     }
     FSVD_TC_BN(128) FSVD_TC_BN(160) FSVD_TC_BN(192) FSVD_TC_BN(224) FSVD_TC_BN(256)
