@@ -46,7 +46,9 @@ struct Cfg {
 };
 
 struct TcArgs {
-    CUtensorMap xmap;  // X [rows][x_ld] bf16, box 64 x 128, SWIZZLE_128B
+    CUtensorMap xmap;     // X [rows][x_ld] bf16, box 64 x 128, SWIZZLE_128B
+    CUtensorMap wmap[3];  // W^T of each segment as {64 el, 16 rows, lines, tiles}: one TMA per stage copies
+                          // line kb of BN/16 tiles verbatim (the layout is already the SW128 image)
     GemmArgs g;
     int seg_tiles[3];  // BN-wide output tiles per segment
     int splits;        // split-K factor (blockIdx.z = split; > 1 only for kGemmStore / kGemmAddF32)
@@ -72,6 +74,14 @@ __device__ __forceinline__ void mbar_wait(uint64_t* b, uint32_t parity) {
         "@!p bra WAIT_%=;\n"
         "}\n" ::"r"(smem_u32(b)),
         "r"(parity)
+        : "memory");
+}
+__device__ __forceinline__ void tma_load_4d(void* dst, const CUtensorMap* map, uint64_t* bar, int c0, int c1, int c2,
+                                            int c3) {
+    asm volatile(
+        "cp.async.bulk.tensor.4d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%3, %4, %5, %6}], "
+        "[%2];" ::"r"(smem_u32(dst)),
+        "l"(map), "r"(smem_u32(bar)), "r"(c0), "r"(c1), "r"(c2), "r"(c3)
         : "memory");
 }
 __device__ __forceinline__ void tma_load_2d(void* dst, const CUtensorMap* map, uint64_t* bar, int c0, int c1) {
@@ -218,9 +228,9 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_tc_kernel(const __grid_const
                 const int kb0 = nk * static_cast<int>(blockIdx.z) / A.splits;
                 const int kb1 = nk * (static_cast<int>(blockIdx.z) + 1) / A.splits;
                 const int t0 = n0 / 16;
-                const int nt = min(BN / 16, lay.ntiles() - t0);
-                const uint32_t bytes = BMT * kABytes + static_cast<uint32_t>(nt) * kLineTileBytes;
-                const char* wbase = static_cast<const char*>(sj.w) + static_cast<size_t>(t0) * lay.tile_bytes();
+                // the W box always lands whole (tiles past the end are zero-filled)
+                const uint32_t bytes = BMT * kABytes + static_cast<uint32_t>(BN / 16) * kLineTileBytes;
+                const CUtensorMap* wm = &A.wmap[DUAL ? j : s];
 #pragma unroll 1
                 for (int kb = kb0; kb < kb1; ++kb, ++it) {
                     const int st = it % C::kStages;
@@ -232,10 +242,7 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_tc_kernel(const __grid_const
 #pragma unroll
                     for (int mi = 0; mi < BMT; ++mi)
                         tma_load_2d(sa + mi * kABytes, &A.xmap, &full[st], sj.x_off + kb * BK, m0 + mi * BM);
-                    const char* wl = wbase + static_cast<size_t>(kb) * kLineTileBytes;
-                    for (int i = 0; i < nt; ++i)
-                        bulk_g2s(sb + i * kLineTileBytes, wl + static_cast<size_t>(i) * lay.tile_bytes(),
-                                 kLineTileBytes, &full[st]);
+                    tma_load_4d(sb, wm, &full[st], 0, 0, kb, t0);
                 }
             }
         }
@@ -298,17 +305,33 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_tc_kernel(const __grid_const
                               valid);
             } else if (A.splits > 1) {  // fp32 partial of this K split (plain store / residual add)
                 float* w = g.ws + (static_cast<size_t>(blockIdx.z) * g.M + t) * g.y_ld + sg.y_off + n;
+                if (valid == 32 && (reinterpret_cast<uintptr_t>(w) & 15) == 0) {  // whole sectors
 #pragma unroll
-                for (int i = 0; i < 32; ++i)
-                    if (i < valid) w[i] = v[i];
+                    for (int i = 0; i < 32; i += 4)
+                        __stcs(reinterpret_cast<float4*>(w + i), make_float4(v[i], v[i + 1], v[i + 2], v[i + 3]));
+                } else {
+#pragma unroll
+                    for (int i = 0; i < 32; ++i)
+                        if (i < valid) w[i] = v[i];
+                }
             } else if (g.epi == kGemmStore) {
                 store_bf16x32(static_cast<__nv_bfloat16*>(g.y) + static_cast<long long>(t) * g.y_ld + sg.y_off + n, v,
                               valid);
             } else if (g.epi == kGemmAddF32) {
                 float* y = static_cast<float*>(g.y) + static_cast<long long>(t) * g.y_ld + sg.y_off + n;
+                if (valid == 32 && (reinterpret_cast<uintptr_t>(y) & 15) == 0) {  // whole sectors
+                    float4 r[8];
 #pragma unroll
-                for (int i = 0; i < 32; ++i)
-                    if (i < valid) y[i] += v[i];
+                    for (int i = 0; i < 8; ++i) r[i] = reinterpret_cast<const float4*>(y)[i];
+#pragma unroll
+                    for (int i = 0; i < 8; ++i)
+                        reinterpret_cast<float4*>(y)[i] = make_float4(r[i].x + v[4 * i], r[i].y + v[4 * i + 1],
+                                                                      r[i].z + v[4 * i + 2], r[i].w + v[4 * i + 3]);
+                } else {
+#pragma unroll
+                    for (int i = 0; i < 32; ++i)
+                        if (i < valid) y[i] += v[i];
+                }
             } else {  // kGemmQKV: RoPE (interleaved pairs, math.hpp:30-44) + q store / KV append
                 const int b = t / g.T, pos = (g.p0_dev ? *g.p0_dev : g.p0) + t % g.T;
                 if (sg.epi != kEpiV) {
@@ -424,6 +447,18 @@ void gemm_tc(const GemmArgs& a, int x_rows, cudaStream_t s) {
                                    CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
     if (r != CUDA_SUCCESS) throw std::runtime_error("cuTensorMapEncodeTiled failed: " + std::to_string(int(r)));
     const bool dual = a.epi == kGemmSilu;
+    auto encode_w = [&](int i, int bn) {
+        const WLayout lay = a.seg[i].layout(2);
+        const cuuint64_t wd[4] = {64, 16, static_cast<cuuint64_t>(lay.nlines()), static_cast<cuuint64_t>(lay.ntiles())};
+        const cuuint64_t ws[3] = {128, static_cast<cuuint64_t>(kLineTileBytes), static_cast<cuuint64_t>(lay.tile_bytes())};
+        const cuuint32_t wb[4] = {64, 16, 1, static_cast<cuuint32_t>(bn / 16)};
+        const cuuint32_t we[4] = {1, 1, 1, 1};
+        const CUresult rw = encode_fn()(&ta.wmap[i], CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 4, const_cast<void*>(a.seg[i].w),
+                                        wd, ws, wb, we, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+                                        CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+        if (rw != CUDA_SUCCESS)
+            throw std::runtime_error("cuTensorMapEncodeTiled (weights) failed: " + std::to_string(int(rw)));
+    };
     const int nseg = dual ? 1 : a.nseg;
     auto count_tiles = [&](int bn) {
         int t = 0;
@@ -495,6 +530,7 @@ void gemm_tc(const GemmArgs& a, int x_rows, cudaStream_t s) {
         tiles += ta.seg_tiles[i];
     }
     ta.splits = best_sp;
+    for (int i = 0; i < a.nseg; ++i) encode_w(i, BN);
     if (std::getenv("FSVD_GEMM_LOG"))
         std::fprintf(stderr, "gemm_tc M=%d N0=%d nseg=%d nk=%d epi=%d -> BN=%d BMT=%d splits=%d tiles=%d\n", a.M,
                      a.seg[0].rows, a.nseg, nk_max, a.epi, BN, best_bmt, best_sp, tiles);
