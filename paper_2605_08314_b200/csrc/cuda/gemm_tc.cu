@@ -217,32 +217,52 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_tc_kernel(const __grid_const
     // K-loop of accumulator j: segment, x column offset, k-blocks
     auto seg_of = [&](int j) -> const GemvSeg& { return DUAL ? g.seg[j] : sg; };
 
+    // Programmatic dependent launch: this grid may start while the previous
+    // kernel drains. Only the weight tiles (constant) are read before
+    // griddepcontrol.wait; activations are read and outputs written after it.
+    asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
     if (warp == 0) {
         if (lane == 0) {
+            auto kb_range = [&](int j, int& kb0, int& kb1) {
+                const int nk = seg_of(j).layout(2).nlines();
+                kb0 = nk * static_cast<int>(blockIdx.z) / A.splits;
+                kb1 = nk * (static_cast<int>(blockIdx.z) + 1) / A.splits;
+            };
+            const int t0 = n0 / 16;
+            // the W box always lands whole (tiles past the end are zero-filled)
+            const uint32_t bytes = BMT * kABytes + static_cast<uint32_t>(BN / 16) * kLineTileBytes;
+            // W tiles of the first ring round, ahead of the grid dependency
+            int npre = 0;
+            for (int j = 0; j < kAcc && npre < C::kStages; ++j) {
+                int kb0, kb1;
+                kb_range(j, kb0, kb1);
+                for (int kb = kb0; kb < kb1 && npre < C::kStages; ++kb, ++npre) {
+                    mbar_expect_tx(&full[npre], bytes);
+                    tma_load_4d(smem + npre * C::kStageBytes + BMT * kABytes, &A.wmap[DUAL ? j : s], &full[npre], 0,
+                                0, kb, t0);
+                }
+            }
+            asm volatile("griddepcontrol.wait;" ::: "memory");
             int it = 0;
 #pragma unroll 1
             for (int j = 0; j < kAcc; ++j) {
                 const GemvSeg& sj = seg_of(j);
-                const WLayout lay = sj.layout(2);
-                const int nk = lay.nlines();
-                const int kb0 = nk * static_cast<int>(blockIdx.z) / A.splits;
-                const int kb1 = nk * (static_cast<int>(blockIdx.z) + 1) / A.splits;
-                const int t0 = n0 / 16;
-                // the W box always lands whole (tiles past the end are zero-filled)
-                const uint32_t bytes = BMT * kABytes + static_cast<uint32_t>(BN / 16) * kLineTileBytes;
                 const CUtensorMap* wm = &A.wmap[DUAL ? j : s];
+                int kb0, kb1;
+                kb_range(j, kb0, kb1);
 #pragma unroll 1
                 for (int kb = kb0; kb < kb1; ++kb, ++it) {
                     const int st = it % C::kStages;
                     const uint32_t ph = (it / C::kStages) & 1;
-                    mbar_wait(&empty[st], ph ^ 1);
                     uint8_t* sa = smem + st * C::kStageBytes;
-                    uint8_t* sb = sa + BMT * kABytes;
-                    mbar_expect_tx(&full[st], bytes);
+                    if (it >= npre) {
+                        mbar_wait(&empty[st], ph ^ 1);
+                        mbar_expect_tx(&full[st], bytes);
+                        tma_load_4d(sa + BMT * kABytes, wm, &full[st], 0, 0, kb, t0);
+                    }
 #pragma unroll
                     for (int mi = 0; mi < BMT; ++mi)
                         tma_load_2d(sa + mi * kABytes, &A.xmap, &full[st], sj.x_off + kb * BK, m0 + mi * BM);
-                    tma_load_4d(sb, wm, &full[st], 0, 0, kb, t0);
                 }
             }
         }
@@ -284,6 +304,7 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_tc_kernel(const __grid_const
         // epilogue: warp w reads TMEM lanes 32*(w%4) .. +31 (= tile rows)
         const int q = warp & 3;
         const int row = q * 32 + lane;
+        asm volatile("griddepcontrol.wait;" ::: "memory");
         mbar_wait(tmem_full, 0);
         tc_fence_after();
 #pragma unroll 1
@@ -388,11 +409,10 @@ EncodeTiled encode_fn() {
 __global__ void __launch_bounds__(256) splitk_reduce_kernel(const __grid_constant__ TcArgs A) {
     const GemmArgs& g = A.g;
     const size_t zs = static_cast<size_t>(g.M) * g.y_ld;  // partial stride
+    const int t = blockIdx.y;
     for (int s = 0; s < g.nseg; ++s) {
         const GemvSeg& sg = g.seg[s];
-        const long long total = static_cast<long long>(g.M) * sg.rows;
-        for (long long i = blockIdx.x * 256ll + threadIdx.x; i < total; i += static_cast<long long>(gridDim.x) * 256) {
-            const int t = static_cast<int>(i / sg.rows), n = static_cast<int>(i - static_cast<long long>(t) * sg.rows);
+        for (int n = blockIdx.x * 256 + threadIdx.x; n < sg.rows; n += gridDim.x * 256) {
             const size_t c = static_cast<size_t>(t) * g.y_ld + sg.y_off + n;
             // all partials' loads in flight (8 at a time), summed in split order
             float acc = 0.f;
@@ -421,8 +441,22 @@ void launch(const TcArgs& ta, int tiles, int M, cudaStream_t s) {
         attr = true;
     }
     dim3 grid((M + BM * BMT - 1) / (BM * BMT), tiles, ta.splits);
-    gemm_tc_kernel<BN, DUAL, BMT><<<grid, kThreads, C::kSmem, s>>>(ta);
-    if (ta.splits > 1) splitk_reduce_kernel<<<4 * 148, 256, 0, s>>>(ta);
+    cudaLaunchConfig_t cfg{};
+    cfg.gridDim = grid;
+    cfg.blockDim = dim3(kThreads);
+    cfg.dynamicSmemBytes = C::kSmem;
+    cfg.stream = s;
+    cudaLaunchAttribute pdl[1];
+    pdl[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    pdl[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = pdl;
+    cfg.numAttrs = std::getenv("FSVD_NO_PDL") ? 0 : 1;
+    cudaLaunchKernelEx(&cfg, gemm_tc_kernel<BN, DUAL, BMT>, ta);
+    if (ta.splits > 1) {
+        int rows = 0;
+        for (int i = 0; i < ta.g.nseg; ++i) rows = std::max(rows, ta.g.seg[i].rows);
+        splitk_reduce_kernel<<<dim3((rows + 255) / 256, M), 256, 0, s>>>(ta);
+    }
 }
 
 }  // namespace

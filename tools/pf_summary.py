@@ -3,8 +3,9 @@ import csv, sys, re, collections
 def load(mode):
     rows = list(csv.reader(open(f"gpurun_out/pf_{mode}.csv")))
     hi = [i for i, r in enumerate(rows) if "Kernel Name" in r][0]
-    h = rows[hi]; ki = h.index("Kernel Name"); vi = h.index("Metric Value")
-    ks = [(r[ki], float(r[vi].replace(",", ""))) for r in rows[hi + 1:] if len(r) > vi]
+    h = rows[hi]; ki = h.index("Kernel Name"); vi = h.index("Metric Value"); mi = h.index("Metric Name")
+    ks = [(r[ki], float(r[vi].replace(",", ""))) for r in rows[hi + 1:]
+          if len(r) > vi and r[mi] == "gpu__time_duration.sum"]
     logs = [l for l in open(f"gpurun_out/pf_{mode}.log") if l.startswith("gemm_tc")]
     return ks, logs
 for mode in sys.argv[1:]:
