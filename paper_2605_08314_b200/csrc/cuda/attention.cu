@@ -129,6 +129,8 @@ __device__ __forceinline__ uint32_t pack_bf16x2(float lo, float hi) {
 
 template <int DH>
 __global__ void __launch_bounds__(kFThreads) attn_prefill_tc_kernel(const __grid_constant__ AttnPrefillArgs a) {
+    pdl_launch_dependents();
+    pdl_wait();
     const int p0 = a.p0_dev ? *a.p0_dev : a.p0;
     constexpr int LD = DH + 8;  // padded smem row (bf16): conflict-free ldmatrix
     extern __shared__ __align__(128) __nv_bfloat16 fsm[];
@@ -284,10 +286,10 @@ void attn_prefill(WType wt, const AttnPrefillArgs& a, cudaStream_t s) {
         const int smem = (kFQ + 4 * kFK) * (a.d_head + 8) * 2;
         if (a.d_head == 128) {
             cudaFuncSetAttribute(attn_prefill_tc_kernel<128>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-            attn_prefill_tc_kernel<128><<<grid, kFThreads, smem, s>>>(a);
+            launch_pdl(attn_prefill_tc_kernel<128>, grid, dim3(kFThreads), smem, s, a);
         } else {
             cudaFuncSetAttribute(attn_prefill_tc_kernel<64>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-            attn_prefill_tc_kernel<64><<<grid, kFThreads, smem, s>>>(a);
+            launch_pdl(attn_prefill_tc_kernel<64>, grid, dim3(kFThreads), smem, s, a);
         }
         return;
     }

@@ -407,6 +407,8 @@ EncodeTiled encode_fn() {
 // Split-K reduction in split order: Y[t][y_off + n] = bf16(sum_z ws[z][t][y_off + n])
 // (plain store) or Yf32[t][y_off + n] += sum_z ws[z][...] (residual add).
 __global__ void __launch_bounds__(256) splitk_reduce_kernel(const __grid_constant__ TcArgs A) {
+    pdl_launch_dependents();
+    pdl_wait();
     const GemmArgs& g = A.g;
     const size_t zs = static_cast<size_t>(g.M) * g.y_ld;  // partial stride
     const int t = blockIdx.y;
@@ -455,7 +457,7 @@ void launch(const TcArgs& ta, int tiles, int M, cudaStream_t s) {
     if (ta.splits > 1) {
         int rows = 0;
         for (int i = 0; i < ta.g.nseg; ++i) rows = std::max(rows, ta.g.seg[i].rows);
-        splitk_reduce_kernel<<<dim3((rows + 255) / 256, M), 256, 0, s>>>(ta);
+        launch_pdl(splitk_reduce_kernel, dim3((rows + 255) / 256, M), dim3(256), 0, s, ta);
     }
 }
 

@@ -47,6 +47,8 @@ __global__ void __launch_bounds__(256) rmsnorm_rows_vec_kernel(const float* x, i
                                                                int d, T* y, int y_ld) {
     constexpr int kIt = 8;
     __shared__ float red[8];
+    pdl_launch_dependents();
+    pdl_wait();
     const float4* xr = reinterpret_cast<const float4*>(x + static_cast<long long>(blockIdx.x) * x_ld);
     const int n4 = d >> 2;
     float4 v[kIt];
@@ -233,10 +235,11 @@ void rmsnorm_rows(WType wt, const float* x, int x_ld, const float* gamma, float 
                      (reinterpret_cast<uintptr_t>(y) & 15) == 0;
     if (vec) {
         if (wt == kBF16)
-            rmsnorm_rows_vec_kernel<__nv_bfloat16><<<rows, 256, 0, s>>>(x, x_ld, gamma, eps, d,
-                                                                          static_cast<__nv_bfloat16*>(y), y_ld);
+            launch_pdl(rmsnorm_rows_vec_kernel<__nv_bfloat16>, dim3(rows), dim3(256), 0, s, x, x_ld, gamma, eps, d,
+                       static_cast<__nv_bfloat16*>(y), y_ld);
         else
-            rmsnorm_rows_vec_kernel<float><<<rows, 256, 0, s>>>(x, x_ld, gamma, eps, d, static_cast<float*>(y), y_ld);
+            launch_pdl(rmsnorm_rows_vec_kernel<float>, dim3(rows), dim3(256), 0, s, x, x_ld, gamma, eps, d,
+                       static_cast<float*>(y), y_ld);
         return;
     }
     if (wt == kBF16)
