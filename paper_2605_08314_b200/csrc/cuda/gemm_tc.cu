@@ -535,24 +535,37 @@ void gemm_tc(const GemmArgs& a, int x_rows, cudaStream_t s) {
             }
         }
     } else {
-        // Prefill (measured per projection on the C2 prompt, ncu launch lists in
-        // profiles/): 128 x 256 tiles when they still cover the SMs, else 128 x 128;
-        // the dual up/gate GEMM at 128 x 160 (2.32 -> 1.86 waves: 128 -> 102 us);
-        // 256 x 256 tiles (two TMEM accumulators sharing each W tile) once the M
-        // tiles alone fill the machine (8192^3: 807 -> 1098 TFLOP/s); split K only
-        // for plain stores whose tiles cover < 1 wave (the reduction costs ~20 us).
-        const int mt = (a.M + BM - 1) / BM;
-        best_bn = count_tiles(256) * mt >= 120 ? 256 : 128;
-        if (dual) best_bn = 160;
-        if (!dual && count_tiles(256) * ((a.M + 2 * BM - 1) / (2 * BM)) >= 148) {
-            best_bn = 256;
-            best_bmt = 2;
-        }
-        if (!dual && a.epi == kGemmStore && a.ws && best_bmt == 1) {
-            int sp = 148 / std::max(1, count_tiles(best_bn) * mt);
-            sp = std::min({sp, 4, nk_min / 4});
-            if (sp > 1 && static_cast<size_t>(sp) * a.M * a.y_ld <= a.ws_floats) best_sp = sp;
-        }
+        // Prefill: a wave model fitted to a sweep of every C2 projection shape at
+        // M = 512 and 2048 (tools/gemm_sweep.cu, profiles/r1_gemm_sweep.md; median
+        // error 9 %, picks within 7.5 % of the best measured config):
+        //   t = waves x (2.06 us + 10.22 us/MB x operand bytes per CTA)
+        //       + [split] (6.61 us + 0.41 us/MB x fp32 partial bytes)
+        // over 128 x {128..256} tiles, 256 x 256 tiles (two TMEM accumulators
+        // sharing each W tile) and 1-4 way split K for plain / residual stores.
+        constexpr int kBNs[] = {128, 160, 192, 224, 256};
+        double best = 1e30;
+        for (int bmt = 1; bmt <= (dual ? 1 : 2); ++bmt)
+            for (int bn : kBNs) {
+                if (bmt == 2 && bn != 256) continue;
+                const int tiles = count_tiles(bn);
+                const int mt = (a.M + BM * bmt - 1) / (BM * bmt);
+                const int max_sp = can_split ? std::max(1, std::min(4, nk_min / 4)) : 1;
+                for (int sp = 1; sp <= max_sp; ++sp) {
+                    if (sp > 1 && static_cast<size_t>(sp) * a.M * a.y_ld > a.ws_floats) break;
+                    const long long ctas = static_cast<long long>(tiles) * mt * sp;
+                    const double waves = static_cast<double>((ctas + 147) / 148);
+                    const double kb = (dual ? 2.0 : 1.0) * nk_max / sp;
+                    const double bytes = kb * (16384.0 * bmt + 128.0 * bn);
+                    double t = waves * (2.06 + 10.22 * bytes / 1e6);
+                    if (sp > 1) t += 6.61 + 0.41 * sp * static_cast<double>(a.M) * a.y_ld * 8.0 / 1e6;
+                    if (t < best * 0.999) {
+                        best = t;
+                        best_bn = bn;
+                        best_sp = sp;
+                        best_bmt = bmt;
+                    }
+                }
+            }
     }
     if (const char* e = std::getenv("FSVD_GEMM_BN")) best_bn = std::atoi(e);
     if (const char* e = std::getenv("FSVD_GEMM_SPLITS"); e && can_split) best_sp = std::max(1, std::atoi(e));
