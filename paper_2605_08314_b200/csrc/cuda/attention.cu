@@ -5,6 +5,8 @@
 // (decode_mk_attn.cuh).
 #include <math_constants.h>
 
+#include <algorithm>
+
 #include "common.cuh"
 #include "kernels.h"
 
@@ -278,7 +280,135 @@ __global__ void __launch_bounds__(kFThreads) attn_prefill_tc_kernel(const __grid
     }
 }
 
+// ---------------------------------------------------------------- decode --
+// Split-KV flash decode for one new query per sequence (batched engine, T = 1):
+// grid (splits, H, B); CTA s takes keys [len*s/S, len*(s+1)/S) of (b, h), its 4
+// warps stream 16-key batches (every K/V load of a batch in flight; lane = 4
+// dims), online softmax per warp (math.hpp:56-101), warps merged in order into
+// a partial (acc, l, m); attn_decode_combine merges the splits in split order.
+constexpr int kDThreads = 128, kDKU = 16;
+
+template <int DH>
+__global__ void __launch_bounds__(kDThreads) attn_decode_kernel(const __grid_constant__ AttnPrefillArgs a, float* part,
+                                                                int S) {
+    constexpr int PER = DH / 32, ST = DH + 2, NW = kDThreads / 32;
+    __shared__ float wst[NW][ST];
+    pdl_launch_dependents();
+    pdl_wait();
+    const int sp = blockIdx.x, h = blockIdx.y, b = blockIdx.z;
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int len = (a.p0_dev ? *a.p0_dev : a.p0) + 1;
+    const int j0 = static_cast<int>(static_cast<long long>(len) * sp / S);
+    const int j1 = static_cast<int>(static_cast<long long>(len) * (sp + 1) / S);
+    const __nv_bfloat16* Kc = static_cast<const __nv_bfloat16*>(a.kcache) + b * a.cache_bstride + h * a.cache_hstride;
+    const __nv_bfloat16* Vc = static_cast<const __nv_bfloat16*>(a.vcache) + b * a.cache_bstride + h * a.cache_hstride;
+    float qr[PER];
+    {
+        const __nv_bfloat16* q = static_cast<const __nv_bfloat16*>(a.q) + static_cast<long long>(b) * a.q_ld + h * DH +
+                                 lane * PER;
+#pragma unroll
+        for (int e = 0; e < PER; ++e) qr[e] = __bfloat162float(q[e]) * a.scale;
+    }
+    float m = -CUDART_INF_F, l = 0.f, acc[PER];
+#pragma unroll
+    for (int e = 0; e < PER; ++e) acc[e] = 0.f;
+    for (int kb = j0 + warp * kDKU; kb < j1; kb += NW * kDKU) {
+        const int k1 = min(kb + kDKU, j1);
+        uint2 kq[kDKU], vq[kDKU];
+#pragma unroll
+        for (int u = 0; u < kDKU; ++u) {
+            const int jj = min(kb + u, k1 - 1);  // clamp: duplicates are masked below
+            kq[u] = __ldcs(reinterpret_cast<const uint2*>(Kc + static_cast<long long>(jj) * DH + lane * PER));
+            vq[u] = __ldcs(reinterpret_cast<const uint2*>(Vc + static_cast<long long>(jj) * DH + lane * PER));
+        }
+        float sc[kDKU];
+        float mb = -CUDART_INF_F;
+#pragma unroll
+        for (int u = 0; u < kDKU; ++u) {
+            float d = qr[0] * bf16lo(kq[u].x);
+            d = fmaf(qr[1], bf16hi(kq[u].x), d);
+            d = fmaf(qr[2], bf16lo(kq[u].y), d);
+            d = fmaf(qr[3], bf16hi(kq[u].y), d);
+            d = warp_sum(d);
+            sc[u] = kb + u < k1 ? d : -CUDART_INF_F;
+            mb = fmaxf(mb, sc[u]);
+        }
+        const float mn = fmaxf(m, mb);
+        const float r = expf(m - mn);
+        l *= r;
+#pragma unroll
+        for (int e = 0; e < PER; ++e) acc[e] *= r;
+#pragma unroll
+        for (int u = 0; u < kDKU; ++u) {
+            const float w = expf(sc[u] - mn);
+            l += w;
+            acc[0] = fmaf(w, bf16lo(vq[u].x), acc[0]);
+            acc[1] = fmaf(w, bf16hi(vq[u].x), acc[1]);
+            acc[2] = fmaf(w, bf16lo(vq[u].y), acc[2]);
+            acc[3] = fmaf(w, bf16hi(vq[u].y), acc[3]);
+        }
+        m = mn;
+    }
+#pragma unroll
+    for (int e = 0; e < PER; ++e) wst[warp][lane * PER + e] = acc[e];
+    if (lane == 0) {
+        wst[warp][DH] = l;
+        wst[warp][DH + 1] = m;
+    }
+    __syncthreads();
+    float M = -CUDART_INF_F;
+#pragma unroll
+    for (int w = 0; w < NW; ++w) M = fmaxf(M, wst[w][DH + 1]);
+    float* dst = part + ((static_cast<long long>(b) * gridDim.y + h) * S + sp) * ST;
+    for (int e = threadIdx.x; e < DH + 1; e += kDThreads) {
+        float t = 0.f;
+#pragma unroll
+        for (int w = 0; w < NW; ++w) {
+            const float mw = wst[w][DH + 1];
+            if (mw != -CUDART_INF_F) t += wst[w][e] * expf(mw - M);
+        }
+        dst[e] = t;
+    }
+    if (threadIdx.x == 0) dst[DH + 1] = M;
+}
+
+template <int DH>
+__global__ void __launch_bounds__(DH) attn_decode_combine(const __grid_constant__ AttnPrefillArgs a, const float* part,
+                                                          int S) {
+    constexpr int ST = DH + 2;
+    pdl_launch_dependents();
+    pdl_wait();
+    const int h = blockIdx.x, b = blockIdx.y, e = threadIdx.x;
+    const float* src = part + (static_cast<long long>(b) * gridDim.x + h) * S * ST;
+    float MM = -CUDART_INF_F;
+    for (int q = 0; q < S; ++q) MM = fmaxf(MM, __ldcg(src + q * ST + DH + 1));
+    float L = 0.f, o = 0.f;
+    for (int q = 0; q < S; ++q) {
+        const float mq = __ldcg(src + q * ST + DH + 1);
+        if (mq == -CUDART_INF_F) continue;  // empty split
+        const float w = expf(mq - MM);
+        L = fmaf(__ldcg(src + q * ST + DH), w, L);
+        o = fmaf(__ldcg(src + q * ST + e), w, o);
+    }
+    static_cast<__nv_bfloat16*>(a.out)[static_cast<long long>(b) * a.out_ld + h * DH + e] = __float2bfloat16_rn(o / L);
+}
+
 }  // namespace
+
+int attn_decode_splits(int batch, int n_heads, int capacity) {
+    // >= 2 CTAs per SM over (B, H), each split >= 64 keys at full capacity
+    int S = (2 * 148 + batch * n_heads - 1) / (batch * n_heads);
+    S = std::min(S, std::max(1, capacity / 64));
+    return std::max(1, std::min(S, 64));
+}
+
+bool attn_decode(WType wt, const AttnPrefillArgs& a, float* part, int S, cudaStream_t s) {
+    if (wt != kBF16 || a.T != 1 || a.d_head != 128 || a.q_ld % 4 || a.out_ld % 2) return false;
+    launch_pdl(attn_decode_kernel<128>, dim3(S, a.n_heads, a.batch), dim3(kDThreads), 0, s, a, part, S);
+    launch_pdl(attn_decode_combine<128>, dim3(a.n_heads, a.batch), dim3(128), 0, s, a, static_cast<const float*>(part),
+               S);
+    return true;
+}
 
 void attn_prefill(WType wt, const AttnPrefillArgs& a, cudaStream_t s) {
     if (wt == kBF16 && (a.d_head == 64 || a.d_head == 128) && a.q_ld % 8 == 0 && a.out_ld % 8 == 0) {

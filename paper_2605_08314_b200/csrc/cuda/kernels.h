@@ -51,6 +51,10 @@ struct AttnPrefillArgs {
     const int* p0_dev;   // non-null: p0 = *p0_dev (graph-replayed batched decode)
 };
 void attn_prefill(WType wt, const AttnPrefillArgs& a, cudaStream_t s);
+// Split-KV flash decode (T = 1, bf16, d_head 128): partials [B][H][S][d_head + 2]
+// fp32 then an in-order merge; false if the shape is not covered.
+int attn_decode_splits(int batch, int n_heads, int capacity);
+bool attn_decode(WType wt, const AttnPrefillArgs& a, float* part, int S, cudaStream_t s);
 
 // ---------------------------------------------------------------- GEMM ----
 // Prefill GEMM: Y[t][n] = epi(sum_k X[t][k] * W^T[n][k]) with X in the weight

@@ -457,6 +457,8 @@ Session::Session(DeviceModel* m, const fsvd_session_opts& o) : m_(m) {
     mk_splits_ = mk_grid_;  // attention partial slots per head: one per contributing CTA
     if (batched_) {
         ensure_prefill_workspace(B_);
+        dec_splits_ = k::attn_decode_splits(B_, static_cast<int>(H), static_cast<int>(cap_));
+        dec_part_ = static_cast<float*>(dalloc(4ull * B_ * H * dec_splits_ * (dh + 2)));
     } else {
         attn_part_ = static_cast<float*>(dalloc(4ull * B_ * H * mk_splits_ * (dh + 2)));
         attn_count_ = static_cast<unsigned*>(dalloc(4ull * B_ * H));
@@ -957,7 +959,9 @@ void Session::layers_forward(int M, int Tc, int p0, const int* p0_dev) {
             a.n_heads = static_cast<int>(c.n_heads);
             a.d_head = static_cast<int>(c.d_head);
             a.scale = static_cast<float>(1.0 / std::sqrt(static_cast<double>(c.d_head)));
-            k::attn_prefill(m.wt, a, stream_);
+            // one new query per sequence (batched decode): split-KV flash decode
+            if (!(Tc == 1 && dec_part_ && k::attn_decode(m.wt, a, dec_part_, dec_splits_, stream_)))
+                k::attn_prefill(m.wt, a, stream_);
         }
         gemm(pf_att_, ldd, 1, {seg(L.at[kO], 0, 0, k::kEpiStore)}, k::kGemmStore, pf_po_, ld_o_);
         gemm(pf_po_, ld_o_, 1, {seg(L.bt[kO], 0, 0, k::kEpiStore)}, k::kGemmAddF32, pf_x_, ldd);

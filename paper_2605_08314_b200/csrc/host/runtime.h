@@ -190,6 +190,8 @@ class Session {
     // with the batch as the M dimension, one graph per step for the graph plans
     bool batched_ = false;
     cudaGraphExec_t bstep_graph_ = nullptr;
+    float* dec_part_ = nullptr;  // split-KV decode attention partials
+    int dec_splits_ = 1;
     int32_t* bstep_out_ = nullptr;
     int bstep_out_ld_ = 0;
 

@@ -109,3 +109,23 @@ def test_batched_capacity_errors(fsvd):
     s.decode_step(np.zeros(4, dtype=np.int32))
     with pytest.raises(fsvd.CapacityError):
         s.decode_step(np.zeros(4, dtype=np.int32))
+
+
+@pytest.mark.parametrize("batch", [3, 16])
+def test_batched_flash_decode_dh128_vs_oracle(fsvd, oracle_mod, batch):
+    """d_head 128 routes the batched decode attention through the split-KV
+    flash-decode kernels (attn_decode); bf16 tolerance, teacher-forced."""
+    cfg = fsvd.ModelConfig(2, 256, 2, 128, 512, 512)
+    spec = fsvd.SynthSpec(cfg, capacity=256, family="A", rho=0.5, seed=13, conditioned=True)
+    rng = np.random.default_rng(batch)
+    prompt = rng.integers(0, cfg.vocab, size=(batch, 70), dtype=np.int32)
+    want, toks = _run_oracle(oracle_mod, spec, prompt, 5)
+    model = fsvd.Model.synthetic(spec, dtype="bf16")
+    for plan in ("eager", "full_step"):
+        s = fsvd.Session(model, batch=batch, capacity=256, plan=plan)
+        got = [s.prefill(prompt)]
+        for i in range(5):
+            got.append(s.decode_step(np.array([toks[b][i] for b in range(batch)], dtype=np.int32)))
+        for b in range(batch):
+            err = max(oracle_mod.rel_err(got[i][b], want[b][i]) for i in range(6))
+            assert err <= TOL["bf16"], (plan, b, err)
