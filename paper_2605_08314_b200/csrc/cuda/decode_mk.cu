@@ -71,7 +71,7 @@ struct GemvShared {
     unsigned ready;                  // warps that published their finalize operands
     int xpf_ok;                      // xpf holds the residual rows of this CTA's tiles
     int nchunks;                     // this CTA's chunks in the phase
-    unsigned released[16];           // rounds of each ring slot consumed so far (whole launch)
+    unsigned released[kMkMaxStages]; // rounds of each ring slot consumed so far (whole launch)
     int pos;                         // length register, read once per launch
     float2 rope[64];                 // kOutQKV: (cos, sin) of position pos
     float xpf[8 * kTileRows * 4];    // kOutResid: residual rows of the CTA's tiles (<= 8 tiles)
@@ -866,7 +866,7 @@ __global__ void __launch_bounds__(kThreads, 1) decode_mk_kernel(const __grid_con
         bulk_g2s_plain(&sm.desc[0], &L.phases[L.p_begin], kDescBytes, &sm.dbar[0]);
     }
     GemvShared& gsh = *static_cast<GemvShared*>(sm.gsh);
-    if (tid < 16) gsh.released[tid] = 0u;
+    if (tid < kMkMaxStages) gsh.released[tid] = 0u;
     {  // this CTA's rows of the chunk tables, once per launch
         const int* cs = L.chunk_start + static_cast<size_t>(cta) * (L.nphases + 1) + L.p_begin;
         const int* ct = L.chunk_tiles + static_cast<size_t>(cta) * L.nphases + L.p_begin;

@@ -155,8 +155,12 @@ struct MkLaunch {
     unsigned long long* trace;  // optional [grid][phases][4] %globaltimer stamps
 };
 
-constexpr int kChunkLines = 8;                       // ring chunk: <= 8 lines of one tile
+#ifndef FSVD_MK_CHUNK_LINES
+#define FSVD_MK_CHUNK_LINES 8
+#endif
+constexpr int kChunkLines = FSVD_MK_CHUNK_LINES;          // ring chunk: <= 8 lines of one tile
 constexpr int kChunkBytes = kChunkLines * kLineTileBytes;  // 16 KiB
+constexpr int kMkMaxStages = 32;                           // ring slots (bounded by shared memory)
 
 // ---- host mirrors of the device work split ----
 // Units (16-row x 128-byte lines) of a GEMV phase.

@@ -704,13 +704,13 @@ void Session::build_program() {
 
     const int dh = static_cast<int>(c.d_head);
     const int nph_all = static_cast<int>(h_phases_.size());
-    mk_stages_ = std::min(12, k::mk_max_stages(x_bytes_, rec_chunks_, B_, dh, nph_all));
+    mk_stages_ = std::min(12 * 8 / k::kChunkLines, k::mk_max_stages(x_bytes_, rec_chunks_, B_, dh, nph_all));
     if (mk_stages_ < 2)
         throw ConfigError("decode megakernel: shared memory does not fit this (batch, shape): x " +
                           std::to_string(x_bytes_) + " B, " + std::to_string(rec_chunks_) + " chunk records");
     mk_smem_ = k::mk_smem_bytes(mk_stages_, x_bytes_, rec_chunks_, B_, dh, nph_all);
     // L2 prefetch distance (chunks per CTA beyond the ring): 16 x 16 KiB x 148 CTAs = 38 MB of the 126 MB L2
-    mk_l2_ahead_ = 8;  // measured best of {0, 8, 16, 24, 32, 48} (C2, B200): 3.07 -> 2.94 ms/token
+    mk_l2_ahead_ = 64 / k::kChunkLines;  // 128 KiB ahead; measured best of {0, 8, 16, 24, 32, 48} (C2, B200): 3.07 -> 2.94 ms/token
     if (const char* e = std::getenv("FSVD_MK_L2_AHEAD")) mk_l2_ahead_ = std::max(0, std::atoi(e));
     if (const char* e = std::getenv("FSVD_MK_PROGRESS"); e && e[0] == '1') {  // hang diagnosis (debug)
         void* h = nullptr;

@@ -5,6 +5,7 @@
 #include <cuda_bf16.h>
 #include <cuda_runtime.h>
 
+#include <algorithm>
 #include <cstdio>
 #include <cstdlib>
 #include <string>
@@ -23,6 +24,7 @@ struct Shape {
 
 int main(int argc, char** argv) {
     const int M = argc > 1 ? atoi(argv[1]) : 512;
+    const int max_sp = argc > 2 ? atoi(argv[2]) : 4;
     const int NC = 6;
     std::vector<Shape> shapes = {
         {"qkvA", {1229, 1229, 1229}, 4096, kGemmStore}, {"qkvB", {4096, 4096, 4096}, 1229, kGemmStore},
@@ -54,7 +56,7 @@ int main(int argc, char** argv) {
         void* y;
         cudaMalloc(&y, size_t(M) * y_ld * 4);
         cudaMemset(y, 0, size_t(M) * y_ld * 4);
-        const size_t wsf = 4ull * M * y_ld;
+        const size_t wsf = static_cast<size_t>(std::max(4, max_sp)) * M * y_ld;
         float* ws;
         cudaMalloc(&ws, wsf * 4);
         auto args = [&](int c) {
@@ -77,10 +79,11 @@ int main(int argc, char** argv) {
         };
         struct Cf { int bn, bmt, sp; };
         std::vector<Cf> cfs;
+        const int spmax = (sh.epi == kGemmStore || sh.epi == kGemmAddF32) ? max_sp : 1;
         for (int bn : {128, 160, 192, 224, 256})
-            for (int sp = 1; sp <= ((sh.epi == kGemmStore || sh.epi == kGemmAddF32) ? 4 : 1); ++sp) cfs.push_back({bn, 1, sp});
-        if (sh.epi != kGemmSilu)
-            for (int sp = 1; sp <= ((sh.epi == kGemmStore || sh.epi == kGemmAddF32) ? 4 : 1); ++sp) cfs.push_back({256, 2, sp});
+            for (int sp = 1; sp <= spmax; sp += (sp < 4 ? 1 : 2)) cfs.push_back({bn, 1, sp});
+        if (sh.epi != kGemmSilu && M > 128)
+            for (int sp = 1; sp <= spmax; ++sp) cfs.push_back({256, 2, sp});
         cfs.push_back({0, 0, 0});  // the library's own choice
         for (const Cf& cf : cfs) {
             if (cf.bn) {

@@ -1,0 +1,3 @@
+nvcc -gencode arch=compute_100a,code=sm_100a -O2 -std=c++20 -I include tools/gemm_sweep.cu -o /tmp/gemm_sweep -L paper_2605_08314_b200 -lfsvd_b200 -Xlinker -rpath=$PWD/paper_2605_08314_b200 || exit 1
+timeout 300 /tmp/gemm_sweep 8 24 > gpurun_out/sweep8.log 2>&1
+timeout 300 /tmp/gemm_sweep 32 24 > gpurun_out/sweep32.log 2>&1
