@@ -251,7 +251,7 @@ __device__ void gemv_phase(const MkGemv& g, const Smem& sm, GemvShared& sh, int 
         fence_proxy_async_global();
         mbar_expect_tx(sm.xbar, xbytes);
         bulk_g2s_plain(sm.x, g.in.p, xbytes, sm.xbar);
-        sh.sp.init(g.seg, g.nseg, g.dual, ES);
+        sh.sp.init(g.seg, g.nseg, g.dual, ES, g.exact_split);
         if (g.out_kind == kOutQKV) {
             // warm L2 with the K/V rows this CTA reads in the attention phase that
             // follows (rows < pos are final; row pos is appended by this phase)
@@ -445,7 +445,9 @@ __device__ void gemv_phase(const MkGemv& g, const Smem& sm, GemvShared& sh, int 
                 }
                 v[sb][b] = acc;
             }
-        // (tile-aligned CTA ranges: every tile has exactly one owner, no exchange)
+        // tile-aligned ranges: one owner per tile; even splits: a shared tile is
+        // finalized by the CTA holding its first unit after the others' pieces
+        if (g.exact_split && !exchange_pieces<B>(g, sp, T, cta, G, lane, v)) continue;
         get_inv();
         finalize_rows<W, B>(g, sh, T, lane, v, inv);
     }
@@ -957,10 +959,10 @@ int mk_out_tiles(const GemvSeg* seg, int nseg, int dual, int esize) {
     return sp.out_tiles;
 }
 
-void mk_split_stats(const GemvSeg* seg, int nseg, int dual, int esize, int grid, int* max_pieces, int* rec_ntl,
-                    int* rec_c0, int* rec_c1) {
+void mk_split_stats(const GemvSeg* seg, int nseg, int dual, int esize, int grid, int exact, int* max_pieces,
+                    int* rec_ntl, int* rec_c0, int* rec_c1) {
     MkSplit sp;
-    sp.init(seg, nseg, dual, esize);
+    sp.init(seg, nseg, dual, esize, exact);
     int mp = 1;
     for (int T = 0; T < sp.out_tiles; ++T) {
         int a, e;
@@ -996,7 +998,7 @@ void mk_build_chunks(const MkPhase* phases, int nphases, int grid, int esize, st
             if (phases[p].kind != kMkGemv) continue;
             const MkGemv& g = phases[p].g;
             MkSplit sp;
-            sp.init(g.seg, g.nseg, g.dual, esize);
+            sp.init(g.seg, g.nseg, g.dual, esize, g.exact_split);
             const int ulo = sp.lo(c, grid), uhi = sp.lo(c + 1, grid);
             if (ulo >= uhi) continue;
             const int Tf = sp.tile_of(ulo);

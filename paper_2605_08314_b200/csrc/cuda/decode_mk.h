@@ -46,6 +46,7 @@ struct MkGemv {
     GemvSeg seg[3];   // weights; seg.x_off = the segment's offset in the input planes
     int nseg;
     int dual;         // seg0 = up, seg1 = gate: per tile, up lines then gate lines
+    int exact_split;  // even unit split over the CTAs; tiles shared by CTAs go through the pieces exchange
     Planes in;
     const float* norm_src;  // non-null: output *= inv_rms(norm_src[b][0..norm_len)) (RMSNorm)
     int norm_ld, norm_len;
@@ -169,8 +170,8 @@ int mk_units(const GemvSeg* seg, int nseg, int dual, int esize);
 int mk_out_tiles(const GemvSeg* seg, int nseg, int dual, int esize);
 // Max CTAs contributing to one output tile; chunk-record shape of a CTA
 // (max local tiles, max chunks per run for sub 0 / 1).
-void mk_split_stats(const GemvSeg* seg, int nseg, int dual, int esize, int grid, int* max_pieces, int* rec_ntl,
-                    int* rec_c0, int* rec_c1);
+void mk_split_stats(const GemvSeg* seg, int nseg, int dual, int esize, int grid, int exact, int* max_pieces,
+                    int* rec_ntl, int* rec_c0, int* rec_c1);
 constexpr int kMkMaxLocalTiles = 64;
 // Chunk records of every GEMV phase for a grid of `grid` CTAs.
 void mk_build_chunks(const struct MkPhase* phases, int nphases, int grid, int esize, std::vector<MkChunk>& out,

@@ -114,10 +114,12 @@ struct MkSplit {
     int ubase[3];
     int ntiles[3], nlines[3], tbase[3];
     int out_tiles;
+    int exact;  // 1: even unit split (tiles may be shared by CTAs: pieces exchange)
 
-    FSVD_HD void init(const GemvSeg* seg, int nseg_, int dual_, int es) {
+    FSVD_HD void init(const GemvSeg* seg, int nseg_, int dual_, int es, int exact_ = 0) {
         nseg = nseg_;
         dual = dual_;
+        exact = exact_;
         int u = 0, t = 0;
         for (int s = 0; s < 3; ++s) {
             ntiles[s] = nlines[s] = tbase[s] = 0;
@@ -149,6 +151,7 @@ struct MkSplit {
         if (c <= 0) return 0;
         if (c >= G) return total;
         const int U = static_cast<int>(static_cast<unsigned>(total) * static_cast<unsigned>(c) / static_cast<unsigned>(G));
+        if (exact) return U;
         int a, e;
         tile_span(tile_of(U), a, e);
         return U - a <= e - U ? a : e;

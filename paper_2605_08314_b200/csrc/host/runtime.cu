@@ -453,7 +453,8 @@ Session::Session(DeviceModel* m, const fsvd_session_opts& o) : m_(m) {
     mk_grid_ = m->sm_count;
     if (const char* g = std::getenv("FSVD_MK_GRID"); g && std::atoi(g) > 0)  // debugging: fewer CTAs
         mk_grid_ = std::min(mk_grid_, std::atoi(g));
-    mk_grid_ = std::min(mk_grid_, 256);  // attention merge scratch is sized for <= 256 pieces per head
+    mk_grid_ = std::min(mk_grid_, 256);
+    if (const char* e = std::getenv("FSVD_MK_EXACT")) mk_exact_ = e[0] == '1';  // attention merge scratch is sized for <= 256 pieces per head
     mk_splits_ = mk_grid_;  // attention partial slots per head: one per contributing CTA
     if (batched_) {
         ensure_prefill_workspace(B_);
@@ -520,8 +521,15 @@ k::MkGemv& Session::add_gemv(const std::vector<k::GemvSeg>& segs, int dual, cons
     g.norm_len = static_cast<int>(m.cfg.d_model);
     g.eps = static_cast<float>(m.cfg.norm_eps);
     g.out_kind = out_kind;
+    // FSVD_MK_EXACT=1: even unit splits (shared boundary tiles through the pieces
+    // exchange) for the long-K rank-space projections, whose few large tiles leave
+    // tile-aligned splits uneven (1 vs 2 tiles per CTA). Measured slower on C2
+    // (3.24 vs 2.90 ms/token: the exchange wait costs more than the imbalance), so
+    // tile-aligned splits are the default.
+    g.exact_split = out_kind == k::kOutPlanes && mk_exact_;
     int max_pieces = 1;
-    k::mk_split_stats(g.seg, g.nseg, dual, m.esize, mk_grid_, &max_pieces, &g.rec_ntl, &g.rec_c0, &g.rec_c1);
+    k::mk_split_stats(g.seg, g.nseg, dual, m.esize, mk_grid_, g.exact_split, &max_pieces, &g.rec_ntl, &g.rec_c0,
+                      &g.rec_c1);
     if (g.rec_ntl > k::kMkMaxLocalTiles)
         throw ConfigError("decode megakernel: a CTA would touch more than 64 output tiles of one phase");
     const int max_chunks = g.rec_ntl * (g.rec_c0 + g.rec_c1);
@@ -529,6 +537,7 @@ k::MkGemv& Session::add_gemv(const std::vector<k::GemvSeg>& segs, int dual, cons
     g.max_pieces = max_pieces;
     g.pieces = static_cast<float*>(dalloc(4ull * nt * max_pieces * 2 * k::kTileRows * B_));
     g.count = static_cast<unsigned*>(dalloc(4ull * nt));
+    FSVD_CUDA(cudaMemsetAsync(g.count, 0, 4ull * nt, stream_));
     rec_chunks_ = std::max(rec_chunks_, max_chunks);
     if (h_phases_.size() == h_phases_.capacity()) throw std::logic_error("phase program capacity");
     h_phases_.push_back(p);
