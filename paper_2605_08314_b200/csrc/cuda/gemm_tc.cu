@@ -387,6 +387,232 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_tc_kernel(const __grid_const
     }
 }
 
+// ------------------------------------------------------ decode (swap AB) --
+// Decode-sized M (<= 64 tokens: the batched engine): the weights are the MMA's
+// A operand (M = 128 output rows per CTA, straight from the W tile box) and the
+// few token rows its B operand (N = NT), so a stage moves 16 KiB of W and only
+// NT x 128 B of X (the 128-row X box of gemm_tc_kernel was 16 KiB of mostly
+// zero-filled rows per k-block). D[row][token] lands in TMEM lanes = output
+// rows; the epilogue writes y[token][row] coalesced across the lanes.
+template <int NT>
+__device__ __forceinline__ void tmem_ld_cols(uint32_t taddr, float (&v)[NT]) {
+    static_assert(NT == 16 || NT == 32, "tcgen05.ld width");
+    if constexpr (NT == 32) {
+        tmem_ld32(taddr, v);
+    } else {
+        uint32_t r[16];
+        asm volatile(
+            "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];"
+            : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]),
+              "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15])
+            : "r"(taddr));
+        asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+#pragma unroll
+        for (int i = 0; i < 16; ++i) v[i] = __uint_as_float(r[i]);
+    }
+}
+
+constexpr int kSwapRows = 128;                   // output rows per CTA (the MMA's M)
+constexpr int kSwapWBytes = kSwapRows * 128;     // W tile per k-block: 16 KiB
+
+template <int NT, bool DUAL>
+__global__ void __launch_bounds__(kThreads, 1) gemm_swap_kernel(const __grid_constant__ TcArgs A) {
+    constexpr int kXBytes = NT * 128;
+    constexpr int kStage = kSwapWBytes + kXBytes;
+    constexpr int kStages = (200 * 1024) / kStage > 12 ? 12 : (200 * 1024) / kStage;
+    constexpr uint32_t kGateCol = 64;  // dual: gate accumulator columns [64, 64 + NT)
+    constexpr uint32_t kAllocCols = DUAL ? 128 : (NT <= 32 ? 32 : 64);
+    extern __shared__ __align__(1024) uint8_t smem_raw[];
+    uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+    uint64_t* full = reinterpret_cast<uint64_t*>(smem + kStages * kStage);
+    uint64_t* empty = full + kStages;
+    uint64_t* tmem_full = empty + kStages;
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tmem_full + 1);
+
+    const GemmArgs& g = A.g;
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    int tile = blockIdx.y, s = 0;
+    if constexpr (!DUAL) {
+        while (s + 1 < g.nseg && tile >= A.seg_tiles[s]) {
+            tile -= A.seg_tiles[s];
+            ++s;
+        }
+    }
+    const GemvSeg& sg = g.seg[s];
+    const int n0 = tile * kSwapRows;
+    constexpr int kAcc = DUAL ? 2 : 1;
+
+    if (threadIdx.x == 0) {
+        for (int i = 0; i < kStages; ++i) {
+            mbar_init(&full[i], 1);
+            mbar_init(&empty[i], 1);
+        }
+        mbar_init(tmem_full, 1);
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+        asm volatile("prefetch.tensormap [%0];" ::"l"(&A.xmap) : "memory");
+    }
+    if (warp == 0) {
+        asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_slot)),
+                     "r"(kAllocCols));
+        asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+    }
+    tc_fence_before();
+    __syncthreads();
+    tc_fence_after();
+    const uint32_t tmem_base = *tmem_slot;
+    auto seg_of = [&](int j) -> const GemvSeg& { return DUAL ? g.seg[j] : sg; };
+    asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+
+    if (warp == 0) {
+        if (lane == 0) {
+            auto kb_range = [&](int j, int& kb0, int& kb1) {
+                const int nk = seg_of(j).layout(2).nlines();
+                kb0 = nk * static_cast<int>(blockIdx.z) / A.splits;
+                kb1 = nk * (static_cast<int>(blockIdx.z) + 1) / A.splits;
+            };
+            const int t0 = n0 / 16;
+            constexpr uint32_t bytes = kStage;
+            int npre = 0;  // W tiles of the first ring round, ahead of the grid dependency
+            for (int j = 0; j < kAcc && npre < kStages; ++j) {
+                int kb0, kb1;
+                kb_range(j, kb0, kb1);
+                for (int kb = kb0; kb < kb1 && npre < kStages; ++kb, ++npre) {
+                    mbar_expect_tx(&full[npre], bytes);
+                    tma_load_4d(smem + npre * kStage, &A.wmap[DUAL ? j : s], &full[npre], 0, 0, kb, t0);
+                }
+            }
+            asm volatile("griddepcontrol.wait;" ::: "memory");
+            int it = 0;
+#pragma unroll 1
+            for (int j = 0; j < kAcc; ++j) {
+                const GemvSeg& sj = seg_of(j);
+                int kb0, kb1;
+                kb_range(j, kb0, kb1);
+#pragma unroll 1
+                for (int kb = kb0; kb < kb1; ++kb, ++it) {
+                    const int st = it % kStages;
+                    const uint32_t ph = (it / kStages) & 1;
+                    uint8_t* sw = smem + st * kStage;
+                    if (it >= npre) {
+                        mbar_wait(&empty[st], ph ^ 1);
+                        mbar_expect_tx(&full[st], bytes);
+                        tma_load_4d(sw, &A.wmap[DUAL ? j : s], &full[st], 0, 0, kb, t0);
+                    }
+                    tma_load_2d(sw + kSwapWBytes, &A.xmap, &full[st], sj.x_off + kb * BK, 0);
+                }
+            }
+        }
+    } else if (warp == 1) {
+        if (lane == 0) {
+            constexpr uint32_t idesc = idesc_bf16<NT>();  // M = 128 (weights), N = NT (tokens)
+            int it = 0;
+#pragma unroll 1
+            for (int j = 0; j < kAcc; ++j) {
+                const int nk = seg_of(j).layout(2).nlines();
+                const int kb0 = nk * static_cast<int>(blockIdx.z) / A.splits;
+                const int kb1 = nk * (static_cast<int>(blockIdx.z) + 1) / A.splits;
+                const uint32_t tacc = tmem_base + static_cast<uint32_t>(j) * kGateCol;
+#pragma unroll 1
+                for (int kb = kb0; kb < kb1; ++kb, ++it) {
+                    const int st = it % kStages;
+                    const uint32_t ph = (it / kStages) & 1;
+                    mbar_wait(&full[st], ph);
+                    tc_fence_after();
+                    const uint32_t sw = smem_u32(smem + st * kStage);
+                    const uint64_t da = sw128_desc(sw), db = sw128_desc(sw + kSwapWBytes);
+#pragma unroll
+                    for (int k = 0; k < BK / 16; ++k)
+                        tc_mma(tacc, da + 2 * k, db + 2 * k, idesc, (kb != kb0 || k != 0) ? 1u : 0u);
+                    tc_commit(&empty[st]);
+                }
+            }
+            tc_commit(tmem_full);
+        }
+    } else {
+        // epilogue: warp q holds output rows n0 + 32 q + lane, NT token columns
+        const int q = warp & 3;
+        const int n = n0 + q * 32 + lane;
+        asm volatile("griddepcontrol.wait;" ::: "memory");
+        mbar_wait(tmem_full, 0);
+        tc_fence_after();
+        const uint32_t lane_addr = tmem_base + (static_cast<uint32_t>(q * 32) << 16);
+        float v[NT], gt[NT];
+        tmem_ld_cols<NT>(lane_addr, v);
+        if constexpr (DUAL) tmem_ld_cols<NT>(lane_addr + kGateCol, gt);
+        const bool ok = n < sg.rows;
+        const int M = g.M;
+        if constexpr (DUAL) {
+            if (ok)
+#pragma unroll
+                for (int t = 0; t < NT; ++t)
+                    if (t < M)
+                        static_cast<__nv_bfloat16*>(g.y)[static_cast<long long>(t) * g.y_ld + sg.y_off + n] =
+                            __float2bfloat16_rn(silu_mul(gt[t], v[t]));
+        } else if (A.splits > 1) {
+            float* w = g.ws + static_cast<size_t>(blockIdx.z) * M * g.y_ld + sg.y_off + n;
+            if (ok)
+#pragma unroll
+                for (int t = 0; t < NT; ++t)
+                    if (t < M) __stcs(w + static_cast<size_t>(t) * g.y_ld, v[t]);
+        } else if (g.epi == kGemmStore) {
+            if (ok)
+#pragma unroll
+                for (int t = 0; t < NT; ++t)
+                    if (t < M)
+                        static_cast<__nv_bfloat16*>(g.y)[static_cast<long long>(t) * g.y_ld + sg.y_off + n] =
+                            __float2bfloat16_rn(v[t]);
+        } else if (g.epi == kGemmAddF32) {
+            if (ok)
+#pragma unroll
+                for (int t = 0; t < NT; ++t)
+                    if (t < M) static_cast<float*>(g.y)[static_cast<long long>(t) * g.y_ld + sg.y_off + n] += v[t];
+        } else {  // kGemmQKV: RoPE on row pairs (2i, 2i+1) = adjacent lanes, math.hpp:30-44
+            const int ih = n % g.d_head;
+            const int p0 = g.p0_dev ? *g.p0_dev : g.p0;
+#pragma unroll
+            for (int t = 0; t < NT; ++t) {
+                const float other = __shfl_xor_sync(0xffffffffu, v[t], 1);
+                if (t >= M || !ok) continue;
+                const int b = t / g.T, pos = p0 + t % g.T;
+                float o = v[t];
+                if (sg.epi != kEpiV) {
+                    const float2 c = g.rope[static_cast<long long>(pos) * (g.d_head / 2) + (ih >> 1)];
+                    o = (ih & 1) ? __fadd_rn(__fmul_rn(other, c.y), __fmul_rn(v[t], c.x))
+                                 : __fsub_rn(__fmul_rn(v[t], c.x), __fmul_rn(other, c.y));
+                }
+                if (sg.epi == kEpiRopeQ) {
+                    static_cast<__nv_bfloat16*>(g.y)[static_cast<long long>(t) * g.y_ld + sg.y_off + n] =
+                        __float2bfloat16_rn(o);
+                } else {
+                    const int h = n / g.d_head;
+                    __nv_bfloat16* c = static_cast<__nv_bfloat16*>(sg.epi == kEpiRopeK ? g.kcache : g.vcache);
+                    c[b * g.cache_bstride + h * g.cache_hstride + static_cast<long long>(pos) * g.d_head + ih] =
+                        __float2bfloat16_rn(o);
+                }
+            }
+        }
+    }
+    tc_fence_before();
+    __syncthreads();
+    if (warp == 0) {
+        tc_fence_after();
+        asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem_base), "r"(kAllocCols));
+    }
+}
+
+template <int NT, bool DUAL>
+void launch_swap(const TcArgs& ta, int tiles, cudaStream_t s) {
+    constexpr int kStage = kSwapWBytes + NT * 128;
+    constexpr int kStages = (200 * 1024) / kStage > 12 ? 12 : (200 * 1024) / kStage;
+    constexpr int kSmem = kStages * kStage + 1024 + 256;
+    static bool attr = false;
+    if (!attr) {
+        cudaFuncSetAttribute(gemm_swap_kernel<NT, DUAL>, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmem);
+        attr = true;
+    }
+    launch_pdl(gemm_swap_kernel<NT, DUAL>, dim3(1, tiles, ta.splits), dim3(kThreads), kSmem, s, ta);
+}
+
 // ------------------------------------------------------------ host side ----
 using EncodeTiled = CUresult (*)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
                                  const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
@@ -476,7 +702,11 @@ void gemm_tc(const GemmArgs& a, int x_rows, cudaStream_t s) {
     ta.g = a;
     const cuuint64_t dims[2] = {static_cast<cuuint64_t>(a.x_ld), static_cast<cuuint64_t>(x_rows)};
     const cuuint64_t strides[1] = {static_cast<cuuint64_t>(a.x_ld) * 2};
-    const cuuint32_t box[2] = {BK, BM};
+    // decode-sized M: the swap-AB kernel (weights as the MMA's M side)
+    // (the QKV epilogue cannot split K: its 96 tiles stream faster as 128 x 256 tiles)
+    const bool swap = a.M <= 32 && a.epi != kGemmQKV && !std::getenv("FSVD_NO_SWAP");
+    const int NT = a.M <= 16 ? 16 : 32;
+    const cuuint32_t box[2] = {BK, static_cast<cuuint32_t>(swap ? NT : BM)};
     const cuuint32_t estr[2] = {1, 1};
     const CUresult r = encode_fn()(&ta.xmap, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(a.x), dims, strides,
                                    box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
@@ -507,6 +737,34 @@ void gemm_tc(const GemmArgs& a, int x_rows, cudaStream_t s) {
         nk_min = std::min(nk_min, a.seg[i].layout(2).nlines());
     }
     const bool can_split = !dual && (a.epi == kGemmStore || a.epi == kGemmAddF32) && a.ws;
+    if (swap) {
+        // 128 output rows per CTA; K split so the CTAs fill one wave (one CTA per
+        // SM: ~200 KiB ring), >= 4 k-blocks per split; deterministic in-order reduction
+        const int tiles = count_tiles(kSwapRows);
+        int sp = 1;
+        if (can_split) {
+            sp = std::max(1, std::min(148 / tiles, nk_min / 4));
+            while (sp > 1 && static_cast<size_t>(sp) * a.M * a.y_ld > a.ws_floats) --sp;
+        }
+        if (const char* e = std::getenv("FSVD_GEMM_SPLITS"); e && can_split) sp = std::max(1, std::atoi(e));
+        for (int i = 0; i < nseg; ++i) ta.seg_tiles[i] = (a.seg[i].rows + kSwapRows - 1) / kSwapRows;
+        for (int i = 0; i < a.nseg; ++i) encode_w(i, kSwapRows);
+        ta.splits = sp;
+        if (std::getenv("FSVD_GEMM_LOG"))
+            std::fprintf(stderr, "gemm_swap M=%d N0=%d nseg=%d nk=%d epi=%d -> NT=%d splits=%d tiles=%d\n", a.M,
+                         a.seg[0].rows, a.nseg, nk_max, a.epi, NT, sp, tiles);
+        if (NT == 16) {
+            if (dual) launch_swap<16, true>(ta, tiles, s); else launch_swap<16, false>(ta, tiles, s);
+        } else {
+            if (dual) launch_swap<32, true>(ta, tiles, s); else launch_swap<32, false>(ta, tiles, s);
+        }
+        if (sp > 1) {
+            int rows = 0;
+            for (int i = 0; i < a.nseg; ++i) rows = std::max(rows, a.seg[i].rows);
+            launch_pdl(splitk_reduce_kernel, dim3((rows + 255) / 256, a.M), dim3(256), 0, s, ta);
+        }
+        return;
+    }
     int best_bn = 128, best_sp = 1, best_bmt = 1;
     if (a.M <= BM) {
         // Decode-sized M (batched engine): the weight stream is the whole cost and
@@ -514,7 +772,7 @@ void gemm_tc(const GemmArgs& a, int x_rows, cudaStream_t s) {
         // model: a CTA streams its k-blocks of 16 KiB X + BN x 128 B of W at
         // ~55 GB/s (measured per-SM L2 -> SM rate), CTAs run in waves of 148, a
         // split adds its partials' round trip and a reduction launch.
-        constexpr int kBNs[] = {128, 160, 192, 224, 256};
+        constexpr int kBNs[] = {64, 96, 128, 160, 192, 224, 256};
         constexpr double kSmRate = 55e9, kHbm = 6.0e12, kLaunch = 3e-6;
         double best = 1e30;
         for (int bn : kBNs) {
@@ -595,7 +853,7 @@ void gemm_tc(const GemmArgs& a, int x_rows, cudaStream_t s) {
             launch<N, false, 1>(ta, tiles, a.M, s);    \
         return;                                        \
     }
-    FSVD_TC_BN(128) FSVD_TC_BN(160) FSVD_TC_BN(192) FSVD_TC_BN(224) FSVD_TC_BN(256)
+    FSVD_TC_BN(64) FSVD_TC_BN(96) FSVD_TC_BN(128) FSVD_TC_BN(160) FSVD_TC_BN(192) FSVD_TC_BN(224) FSVD_TC_BN(256)
 #undef FSVD_TC_BN
     throw std::runtime_error("gemm_tc: unsupported tile width " + std::to_string(BN));
 }

@@ -80,7 +80,7 @@ int main(int argc, char** argv) {
         struct Cf { int bn, bmt, sp; };
         std::vector<Cf> cfs;
         const int spmax = (sh.epi == kGemmStore || sh.epi == kGemmAddF32) ? max_sp : 1;
-        for (int bn : {128, 160, 192, 224, 256})
+        for (int bn : {64, 96, 128, 160, 192, 224, 256})
             for (int sp = 1; sp <= spmax; sp += (sp < 4 ? 1 : 2)) cfs.push_back({bn, 1, sp});
         if (sh.epi != kGemmSilu && M > 128)
             for (int sp = 1; sp <= spmax; ++sp) cfs.push_back({256, 2, sp});

@@ -1,0 +1,6 @@
+nvcc -gencode arch=compute_100a,code=sm_100a -O2 -std=c++20 -I include tools/gemm_sweep.cu -o /tmp/gemm_sweep -L paper_2605_08314_b200 -lfsvd_b200 -Xlinker -rpath=$PWD/paper_2605_08314_b200 || exit 1
+timeout 300 /tmp/gemm_sweep 8 24 > gpurun_out/sweep8b.log 2>&1
+grep -E "^ugB|auto" gpurun_out/sweep8b.log | head -30
+timeout 900 python -m pytest tests/test_gpu_batched.py -x -q 2>&1 | tail -2
+timeout 600 python bench.py --config c3 --steps 1 --warmup 3 --gen 64 --no-cpu-baseline > gpurun_out/pf_c3.log 2>&1
+python -c "import json; j=json.loads(open('gpurun_out/pf_c3.log').read().strip().splitlines()[-1]); print('c3 decode', round(j['decode_ms_per_token'],3), 'frac', round(j['roofline']['frac'],3))"
