@@ -96,7 +96,7 @@ __global__ void __launch_bounds__(kPThreads) attn_prefill_kernel(const __grid_co
 // 64-key tiles double-buffered in shared memory with cp.async; S = Q.K^T and
 // O += P.V on the tensor cores (mma.sync m16n8k16, fp32 accumulate), online
 // softmax in registers (the running-max recurrence of math.hpp:75-100).
-constexpr int kFQ = 64, kFK = 64, kFThreads = 128;
+constexpr int kFQ = 64, kFK = 64, kFThreads = kFQ / 16 * 32;  // 16 queries per warp
 
 __device__ __forceinline__ uint32_t smem_addr(const void* p) {
     return static_cast<uint32_t>(__cvta_generic_to_shared(p));
@@ -139,7 +139,8 @@ __global__ void __launch_bounds__(kFThreads) attn_prefill_tc_kernel(const __grid
     __nv_bfloat16* Qs = fsm;                 // [kFQ][LD]
     __nv_bfloat16* Ks = Qs + kFQ * LD;       // [2][kFK][LD]
     __nv_bfloat16* Vs = Ks + 2 * kFK * LD;   // [2][kFK][LD]
-    const int qt = blockIdx.x, h = blockIdx.y, b = blockIdx.z;
+    // causal work grows with the query tile: the heaviest tiles are scheduled first
+    const int qt = gridDim.x - 1 - blockIdx.x, h = blockIdx.y, b = blockIdx.z;
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31, g = lane >> 2, t4 = lane & 3;
     const int q0 = qt * kFQ;
     const __nv_bfloat16* Q = static_cast<const __nv_bfloat16*>(a.q) + static_cast<long long>(b) * a.T * a.q_ld + h * DH;
