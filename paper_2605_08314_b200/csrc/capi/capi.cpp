@@ -352,12 +352,11 @@ fsvd_status fsvd_decode_step(fsvd_session* s, const int32_t* tokens, float* logi
         auto& S = *s->s;
         const size_t B = S.batch(), V = S.vocab();
         const size_t tok_bytes = B * 4, log_bytes = B * V * 4;
-        char* stage = static_cast<char*>(S.staging(tok_bytes + log_bytes + 256));
-        int32_t* d_tok = reinterpret_cast<int32_t*>(stage);
-        float* d_log = reinterpret_cast<float*>(stage + 256);
+        int32_t* d_tok = static_cast<int32_t*>(S.staging(tok_bytes));
         FSVD_CUDA(cudaMemcpyAsync(d_tok, tokens, tok_bytes, cudaMemcpyHostToDevice, S.stream()));
-        S.decode_step(d_tok, d_log);
-        if (logits_out) FSVD_CUDA(cudaMemcpyAsync(logits_out, d_log, log_bytes, cudaMemcpyDeviceToHost, S.stream()));
+        S.decode_step(d_tok, nullptr);  // logits stay in the session buffer: one D2H copy, no staging hop
+        if (logits_out)
+            FSVD_CUDA(cudaMemcpyAsync(logits_out, S.logits_device(), log_bytes, cudaMemcpyDeviceToHost, S.stream()));
         FSVD_CUDA(cudaStreamSynchronize(S.stream()));
         S.stats().copy_bytes += tok_bytes + (logits_out ? log_bytes : 0);
     });

@@ -99,6 +99,7 @@ class Session {
     void read_kv(size_t layer, size_t b, int which, size_t pos0, size_t npos, float* out);
 
     size_t position() const { return position_; }
+    const float* logits_device() const { return logits_; }  // [B][V] of the last prefill / decode step
     int batch() const { return B_; }
     int vocab() const { return static_cast<int>(m_->cfg.vocab); }
     cudaStream_t stream() const { return stream_; }
