@@ -263,8 +263,7 @@ def run_ours(args):
         sess.prefill_device(prompts.data_ptr(), P)
         if ev:
             ev[1].record(stream)
-        for _ in range(G):
-            sess.decode_step_device()
+        sess.decode_steps_device(G)  # G greedy steps on the device (megakernel: one launch per <= 256 steps)
         if ev:
             ev[2].record(stream)
 
@@ -380,7 +379,7 @@ def run_ours(args):
         # our kernels in the timed region, per request: prefill = embed + per layer (2 RMSNorm,
         # 8 tcgen05 GEMMs, 1 flash attention, 2 split-K reductions at prompt 512) + gather + 2
         # length-register sets + the head/argmax megakernel; decode = one full-step megakernel
-        # launch (one CUDA graph) per token
+        # launch per <= 256 tokens (decode_steps_device; the phase program repeated inside the launch)
         if engine.get("batched"):
             # batched engine: prefill as above with the head as norm + GEMM + argmax + advance
             # (5 launches); decode per token = embed + per layer (2 RMSNorm, 8 GEMMs, <= 6
@@ -389,7 +388,8 @@ def run_ours(args):
             line["gpu_launches"] = args.steps * (prefill_launches + G * (1 + L * 17 + 5))
         else:
             prefill_launches = 1 + L * (2 + 8 + 1 + (2 if P <= 1024 else 0)) + 1 + 2 + 1
-            line["gpu_launches"] = args.steps * (prefill_launches + G * (1 if args.plan == "full_step" else L + 2))
+            line["gpu_launches"] = args.steps * (prefill_launches + ((G + 255) // 256 if args.plan == "full_step"
+                                                                     else G * (L + 2)))
         tf = ROOT / "profiles" / "traffic.json"
         if tf.exists():  # dram bytes of one full-step decode launch from an ncu --set full capture
             try:

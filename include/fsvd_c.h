@@ -148,6 +148,10 @@ fsvd_status fsvd_prefill_device(fsvd_session* s, const int32_t* d_tokens, uint64
 fsvd_status fsvd_decode_step_device(fsvd_session* s, const int32_t* d_tokens, float* d_logits);
 fsvd_status fsvd_generate_device(fsvd_session* s, const int32_t* d_prompt, uint64_t T, uint64_t max_new,
                                  int32_t* d_out);
+/* n greedy decode steps continuing from the last argmax (no host round trip);
+ * d_out: [batch][n] generated tokens or NULL; logits of the last step stay on the
+ * session. Extension of SPEC.md:341-349 generate for a serving loop. */
+fsvd_status fsvd_decode_steps_device(fsvd_session* s, uint64_t n, int32_t* d_out);
 fsvd_status fsvd_session_sync(fsvd_session* s);
 fsvd_status fsvd_session_stream(fsvd_session* s, void** cuda_stream);
 fsvd_status fsvd_session_position(const fsvd_session* s, uint64_t* position);

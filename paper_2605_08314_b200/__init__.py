@@ -193,6 +193,7 @@ def lib() -> C.CDLL:
         "fsvd_generate": ([vp, i32p, u64, u64, i32p], C.c_int),
         "fsvd_prefill_device": ([vp, vp, u64, vp], C.c_int),
         "fsvd_decode_step_device": ([vp, vp, vp], C.c_int),
+        "fsvd_decode_steps_device": ([vp, C.c_uint64, vp], C.c_int),
         "fsvd_generate_device": ([vp, vp, u64, u64, vp], C.c_int),
         "fsvd_session_sync": ([vp], C.c_int),
         "fsvd_session_stream": ([vp, C.POINTER(vp)], C.c_int),
@@ -220,7 +221,7 @@ def exported_symbols() -> list[str]:
             "fsvd_synthetic_write_file", "fsvd_model_load", "fsvd_model_from_canonical", "fsvd_model_synthetic",
             "fsvd_model_info", "fsvd_model_copy_factor", "fsvd_model_destroy", "fsvd_route_ffn_auto",
             "fsvd_session_create", "fsvd_prefill", "fsvd_decode_step", "fsvd_generate", "fsvd_prefill_device",
-            "fsvd_decode_step_device", "fsvd_generate_device", "fsvd_session_sync", "fsvd_session_stream",
+            "fsvd_decode_step_device", "fsvd_decode_steps_device", "fsvd_generate_device", "fsvd_session_sync", "fsvd_session_stream",
             "fsvd_session_position", "fsvd_session_reset", "fsvd_session_stats", "fsvd_session_resolved",
             "fsvd_session_read_kv", "fsvd_session_engine", "fsvd_session_trace", "fsvd_session_destroy"]
 
@@ -418,6 +419,10 @@ class Session:
 
     def decode_step_device(self, d_tokens: int = 0, d_logits: int = 0) -> None:
         _check(lib().fsvd_decode_step_device(self._h, C.c_void_p(d_tokens or None), C.c_void_p(d_logits or None)))
+
+    def decode_steps_device(self, n: int, d_out: int = 0) -> None:
+        """n greedy decode steps on the device (megakernel: one launch per <= 256 steps)."""
+        _check(lib().fsvd_decode_steps_device(self._h, n, C.c_void_p(d_out or None)))
 
     def generate_device(self, d_prompt: int, T: int, max_new: int, d_out: int) -> None:
         _check(lib().fsvd_generate_device(self._h, C.c_void_p(d_prompt), T, max_new, C.c_void_p(d_out)))

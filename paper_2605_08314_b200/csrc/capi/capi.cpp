@@ -396,6 +396,13 @@ fsvd_status fsvd_decode_step_device(fsvd_session* s, const int32_t* d_tokens, fl
     });
 }
 
+fsvd_status fsvd_decode_steps_device(fsvd_session* s, uint64_t n, int32_t* d_out) {
+    return guarded([&] {
+        need(s, "session");
+        s->s->decode_steps(n, d_out, static_cast<int>(n));
+    });
+}
+
 fsvd_status fsvd_generate_device(fsvd_session* s, const int32_t* d_prompt, uint64_t T, uint64_t max_new,
                                  int32_t* d_out) {
     return guarded([&] {

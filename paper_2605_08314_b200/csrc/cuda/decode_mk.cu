@@ -820,6 +820,7 @@ __global__ void __launch_bounds__(kThreads, 1) decode_mk_kernel(const __grid_con
         }
         uint4* meta = reinterpret_cast<uint4*>(sm.meta);
         uint32_t seq = 0;
+        for (int rep = 0; rep < (L.reps > 1 ? L.reps : 1); ++rep)
         for (int ib = i0; ib < i1; ib += 32) {
             uint4 rec = make_uint4(0u, 0u, 0u, 0u);
             if (ib + lane < i1) rec = __ldg(reinterpret_cast<const uint4*>(L.chunks + ib + lane));
@@ -881,29 +882,33 @@ __global__ void __launch_bounds__(kThreads, 1) decode_mk_kernel(const __grid_con
     consumer_sync();
     uint32_t cseq = 0, xphase = 0;
     const int nph = L.p_end - L.p_begin;
-    for (int p = L.p_begin; p < L.p_end; ++p) {
-        const int idx = p - L.p_begin, buf = idx & 1;
+    // reps > 1: the phase program runs reps times back to back (reps decode steps
+    // in one launch); gi counts phases over the whole launch
+    const int reps = L.reps > 1 ? L.reps : 1, ntot = nph * reps;
+    for (int gi = 0; gi < ntot; ++gi) {
+        const int idx = gi % nph, p = L.p_begin + idx, buf = gi & 1;
         unsigned long long* tr = L.trace ? L.trace + (static_cast<size_t>(cta) * nph + idx) * 16 : nullptr;
         if (L.progress && tid == 0) {
             L.progress[cta * 16] = p;
             L.progress[cta * 16 + 1] = 0;
         }
-        if (idx > 0) {  // grid barrier: every CTA finished phase idx-1
+        if (gi > 0) {  // grid barrier: every CTA finished phase gi-1
             if (tid == 0) {
-                const unsigned target = static_cast<unsigned>(idx) * G;
+                const unsigned target = static_cast<unsigned>(gi) * G;
                 while (ld_acquire(L.bar) < target) {
                 }
+                if (idx == 0) gsh.pos = L.pos ? __ldcg(L.pos) : 0;  // next step: the argmax phase advanced it
             }
             consumer_sync();
         }
-        if (tid == 0 && p + 1 < L.p_end) {  // prefetch the next descriptor (its buffer's readers are done)
+        if (tid == 0 && gi + 1 < ntot) {  // prefetch the next descriptor (its buffer's readers are done)
             asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
             mbar_expect_tx(&sm.dbar[buf ^ 1], kDescBytes);
-            bulk_g2s_plain(&sm.desc[buf ^ 1], &L.phases[p + 1], kDescBytes, &sm.dbar[buf ^ 1]);
+            bulk_g2s_plain(&sm.desc[buf ^ 1], &L.phases[L.p_begin + (gi + 1) % nph], kDescBytes, &sm.dbar[buf ^ 1]);
         }
         if (tr && tid == 0) for (int q = 0; q < 16; ++q) if (q != 5 && q != 6) tr[q] = gtimer();
         if (L.progress && tid == 0) L.progress[cta * 16 + 1] = 1;
-        mbar_wait(&sm.dbar[buf], (idx >> 1) & 1u);
+        mbar_wait(&sm.dbar[buf], (gi >> 1) & 1u);
         if (L.progress && tid == 0) L.progress[cta * 16 + 1] = 2;
         const MkPhase& ph = sm.desc[buf];
         switch (ph.kind) {
@@ -916,12 +921,12 @@ __global__ void __launch_bounds__(kThreads, 1) decode_mk_kernel(const __grid_con
         consumer_sync();
         if (L.progress && tid == 0) L.progress[cta * 16 + 1] = 4;
         if (tr && tid == 0) tr[4] = gtimer();
-        if (tid == 0) {  // arrive (release): this CTA's writes of phase idx are complete
-            if (idx + 1 < nph) {
+        if (tid == 0) {  // arrive (release): this CTA's writes of phase gi are complete
+            if (gi + 1 < ntot) {
                 red_release_add(L.bar, 1u);  // fire and forget
             } else {
                 const unsigned v = atom_add_acq_rel(L.bar, 1u) + 1u;
-                if (v == static_cast<unsigned>(nph) * G) *L.bar = 0u;  // last arrival of the launch: reset
+                if (v == static_cast<unsigned>(ntot) * G) *L.bar = 0u;  // last arrival of the launch: reset
             }
         }
     }

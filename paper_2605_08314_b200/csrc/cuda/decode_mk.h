@@ -141,6 +141,7 @@ struct alignas(16) MkChunk {
 struct MkLaunch {
     const MkPhase* phases;  // device array
     int p_begin, p_end;
+    int reps;               // >= 1: run phases [p_begin, p_end) reps times (multi-step decode launch)
     unsigned* bar;          // zero-initialized grid-barrier counter (self-resetting)
     int grid, smem_bytes;
     int stages;             // ring depth (kChunkBytes each)

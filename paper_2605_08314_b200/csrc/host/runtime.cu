@@ -760,11 +760,12 @@ void Session::build_program() {
                               cudaMemcpyHostToDevice, stream_));
 }
 
-void Session::mk_run(int p_begin, int p_end) {
+void Session::mk_run(int p_begin, int p_end, int reps) {
     k::MkLaunch L{};
     L.phases = d_phases_;
     L.p_begin = p_begin;
     L.p_end = p_end;
+    L.reps = reps;
     L.bar = mk_bar_;
     L.grid = mk_grid_;
     L.smem_bytes = mk_smem_;
@@ -778,7 +779,7 @@ void Session::mk_run(int p_begin, int p_end) {
     L.chunk_tiles = d_chunk_tiles_;
     L.nphases = static_cast<int>(h_phases_.size());
     L.progress = mk_progress_;
-    if (trace_ && p_begin == 0 && p_end == ph_argmax_ + 1) L.trace = trace_;
+    if (trace_ && p_begin == 0 && p_end == ph_argmax_ + 1 && reps == 1) L.trace = trace_;
     if (!k::mk_launch(m_->wt, B_, static_cast<int>(m_->cfg.d_head), L, stream_))
         throw CudaError("megakernel: no instantiation for this (dtype, batch, d_head)");
     FSVD_CUDA(cudaGetLastError());
@@ -865,6 +866,36 @@ void Session::decode_step(const int32_t* d_tokens, float* d_logits) {
     stats_.last_dispatches = stats_.dispatches - before;
     stats_.steps += 1;
     position_ += 1;
+}
+
+// n greedy decode steps without host round trips (each feeds back its argmax).
+// Megakernel + full-step plan: one launch runs up to 256 steps (the phase
+// program repeated, pos re-read after each step's argmax): no per-token launch
+// gap. Other engines / plans: n single steps. Bitwise identical either way.
+void Session::decode_steps(size_t n, int32_t* d_out, int out_ld) {
+    if (n == 0) return;
+    if (position_ == 0) throw ShapeError("decode_steps: prefill first (position = 0)");
+    if (position_ + n > cap_)
+        throw CapacityError("decode_steps: " + std::to_string(n) + " steps exceed capacity " + std::to_string(cap_));
+    const uint64_t before = stats_.dispatches;
+    if (d_out) k::set_int(step_, 0, stream_);  // tokens land in columns 0 .. n-1
+    if (batched_ || plan_ != FSVD_PLAN_FULL_STEP) {
+        for (size_t i = 0; i < n; ++i) decode_any(d_out, out_ld);
+    } else {
+        mk_set_out(d_out, out_ld);
+        for (size_t i = 0; i < n;) {
+            const int r = static_cast<int>(std::min<size_t>(256, n - i));
+            launches_this_step_ = 0;
+            mk_run(0, ph_argmax_ + 1, r);
+            stats_.dispatches += 1;
+            stats_.kernel_launches += 1;
+            i += r;
+        }
+    }
+    FSVD_CUDA(cudaGetLastError());
+    stats_.last_dispatches = (stats_.dispatches - before) / n;
+    stats_.steps += n;
+    position_ += n;
 }
 
 // --------------------------------------------------------------- prefill --

@@ -95,6 +95,8 @@ class Session {
     void prefill(const int32_t* d_tokens, size_t T, float* d_logits);  // device pointers
     void decode_step(const int32_t* d_tokens, float* d_logits);        // d_tokens may be null: use last argmax
     void generate(const int32_t* d_prompt, size_t T, size_t max_new, int32_t* d_out);
+    // n greedy steps from the last argmax, on the device; d_out [B][out_ld] at columns *step.. (may be null)
+    void decode_steps(size_t n, int32_t* d_out, int out_ld);
     void reset();
     void read_kv(size_t layer, size_t b, int which, size_t pos0, size_t npos, float* out);
 
@@ -120,7 +122,7 @@ class Session {
   private:
     void build_program();
     void add_layer_phases(size_t l, const float* next_gamma);
-    void mk_run(int p_begin, int p_end);
+    void mk_run(int p_begin, int p_end, int reps = 1);
     void mk_decode(int32_t* d_out, int out_ld);
     void mk_set_out(int32_t* d_out, int out_ld);
     void prefill_chunk(const int32_t* d_tokens, size_t T_total, size_t t0, size_t Tc);
