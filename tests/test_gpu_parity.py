@@ -243,3 +243,32 @@ def test_batch_prefill_decode_bf16_matches_oracle(fsvd, oracle_mod):
         os_ = om.session(f64=True, capacity=512)
         assert oracle_mod.rel_err(lp[b], os_.prefill(prompt[b])) <= 2e-2
         assert oracle_mod.rel_err(ld[b], os_.decode_step(int(nxt[b]))) <= 2e-2
+
+
+@pytest.mark.parametrize("batch", [1, 2, 4])
+def test_llama7b_shape_two_layers_vs_oracle(fsvd, oracle_mod, batch):
+    """The bench's real layer shapes (d 4096, 32 heads x 128, d_ff 11008, V 32000,
+    rho 0.6 -> ranks 1229 / 1791) for 2 layers: megakernel (B <= 2) and batched
+    engine (B = 4) vs the f64 oracle, bf16 tolerance; exercises the production
+    tile splits, ring chunking and the tcgen05 prefill tiles at full size."""
+    base, _ = fsvd.PRESETS["llama7b"]
+    cfg = fsvd.ModelConfig(2, base.d_model, base.n_heads, base.d_head, base.d_ff, base.vocab)
+    spec = fsvd.SynthSpec(cfg, capacity=64, family="A", rho=0.6, seed=3, conditioned=True)
+    prompt = _prompt(cfg, 9, seed=5, batch=batch)
+    om = oracle_mod.OracleModel.synthetic(spec)
+    model = fsvd.Model.synthetic(spec, dtype="bf16")
+    s = fsvd.Session(model, batch=batch, capacity=64, plan="full_step")
+    got = [s.prefill(prompt)]
+    nxt = np.argmax(got[0], axis=1).astype(np.int32)
+    for _ in range(2):
+        got.append(s.decode_step(nxt))
+        nxt = np.argmax(got[-1], axis=1).astype(np.int32)
+    for b in range(batch):
+        os_ = om.session(f64=True, capacity=64)
+        want = [os_.prefill(prompt[b])]
+        tok = int(np.argmax(got[0][b]))
+        for i in range(2):
+            want.append(os_.decode_step(tok))
+            tok = int(np.argmax(got[i + 1][b]))
+        errs = [oracle_mod.rel_err(got[i][b], want[i]) for i in range(3)]
+        assert max(errs) <= TOL["bf16"], (b, errs)
