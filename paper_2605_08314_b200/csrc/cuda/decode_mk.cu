@@ -252,25 +252,6 @@ __device__ void gemv_phase(const MkGemv& g, const Smem& sm, GemvShared& sh, int 
         mbar_expect_tx(sm.xbar, xbytes);
         bulk_g2s_plain(sm.x, g.in.p, xbytes, sm.xbar);
         sh.sp.init(g.seg, g.nseg, g.dual, ES, g.exact_split);
-        if (g.out_kind == kOutQKV) {
-            // warm L2 with the K/V rows this CTA reads in the attention phase that
-            // follows (rows < pos are final; row pos is appended by this phase)
-            const int H = g.seg[0].rows / g.d_head, len = sh.pos + 1;
-            const RowSplit rs{B * H * len};
-            const int r0 = rs.lo(cta, G), r1 = rs.lo(cta + 1, G);
-            for (int bh = r0 / len; r1 > r0 && bh <= (r1 - 1) / len; ++bh) {
-                const int j0 = max(r0 - bh * len, 0), j1 = min(r1 - bh * len, len - 1);
-                if (j1 <= j0) continue;
-                const long long off = (bh / H) * g.cache_bstride + (bh % H) * g.cache_hstride +
-                                      static_cast<long long>(j0) * g.d_head;
-                const uint32_t bytes = static_cast<uint32_t>(j1 - j0) * g.d_head * ES;
-                for (uint32_t o = 0; o < bytes; o += 16384u) {
-                    const uint32_t n = min(16384u, bytes - o);
-                    prefetch_l2_bulk(static_cast<const char*>(g.kcache) + off * ES + o, n);
-                    prefetch_l2_bulk(static_cast<const char*>(g.vcache) + off * ES + o, n);
-                }
-            }
-        }
         sh.Tf = Tf;
         sh.xpf_ok = g.out_kind == kOutResid && Tl >= Tf && (Tl - Tf + 1) * kTileRows <= 8 * kTileRows;
         sh.next = 0u;
@@ -285,6 +266,26 @@ __device__ void gemv_phase(const MkGemv& g, const Smem& sm, GemvShared& sh, int 
         for (int q = tid; q < n4; q += kConsumerThreads) r4[q] = make_float4(0.f, 0.f, 0.f, 0.f);
     }
     consumer_sync();
+    if (g.out_kind == kOutQKV && tid == kConsumerThreads - 32) {  // (off tid 0's staging path)
+        // warm L2 with the K/V rows this CTA reads in the attention phase that
+        // follows (rows < pos are final; row pos is appended by this phase)
+        const int H = g.seg[0].rows / g.d_head, len = sh.pos + 1;
+        const RowSplit rs{B * H * len};
+        const int r0 = rs.lo(cta, G), r1 = rs.lo(cta + 1, G);
+        for (int bh = r0 / len; r1 > r0 && bh <= (r1 - 1) / len; ++bh) {
+            const int j0 = max(r0 - bh * len, 0), j1 = min(r1 - bh * len, len - 1);
+            if (j1 <= j0) continue;
+            const long long off = (bh / H) * g.cache_bstride + (bh % H) * g.cache_hstride +
+                                  static_cast<long long>(j0) * g.d_head;
+            const uint32_t bytes = static_cast<uint32_t>(j1 - j0) * g.d_head * ES;
+            for (uint32_t o = 0; o < bytes; o += 16384u) {
+                const uint32_t n = min(16384u, bytes - o);
+                prefetch_l2_bulk(static_cast<const char*>(g.kcache) + off * ES + o, n);
+                prefetch_l2_bulk(static_cast<const char*>(g.vcache) + off * ES + o, n);
+            }
+        }
+    }
+
     // issue the operand loads (registers), consumed after the x copy lands
     float2 rope_v = make_float2(0.f, 0.f);
     const bool has_rope = g.out_kind == kOutQKV && tid < g.d_head / 2;
