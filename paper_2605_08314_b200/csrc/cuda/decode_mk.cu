@@ -246,11 +246,7 @@ __device__ void gemv_phase(const MkGemv& g, const Smem& sm, GemvShared& sh, int 
     // ---- stage the input planes (one bulk copy); the finalize operands (RMSNorm
     // sum of squares, RoPE row, residual rows) load in the shadow of that copy ----
     const int Tf = tinfo >= 0 ? (tinfo & 0xFFFF) : 0, Tl = tinfo >= 0 ? (tinfo >> 16) : -1;
-    if (tid == 0) {
-        const uint32_t xbytes = static_cast<uint32_t>(B) * g.in.len * PlaneIO<W>::kBytesPerElem;
-        fence_proxy_async_global();
-        mbar_expect_tx(sm.xbar, xbytes);
-        bulk_g2s_plain(sm.x, g.in.p, xbytes, sm.xbar);
+    if (tid == 0) {  // (the input planes' bulk copy was issued by the main loop right after the barrier)
         sh.sp.init(g.seg, g.nseg, g.dual, ES, g.exact_split);
         sh.Tf = Tf;
         sh.xpf_ok = g.out_kind == kOutResid && Tl >= Tf && (Tl - Tf + 1) * kTileRows <= 8 * kTileRows;
@@ -893,15 +889,25 @@ __global__ void __launch_bounds__(kThreads, 1) decode_mk_kernel(const __grid_con
             L.progress[cta * 16] = p;
             L.progress[cta * 16 + 1] = 0;
         }
-        if (gi > 0) {  // grid barrier: every CTA finished phase gi-1
-            if (tid == 0) {
+        if (tid == 0) {
+            if (gi > 0) {  // grid barrier: every CTA finished phase gi-1
                 const unsigned target = static_cast<unsigned>(gi) * G;
                 while (ld_acquire(L.bar) < target) {
                 }
                 if (idx == 0) gsh.pos = L.pos ? __ldcg(L.pos) : 0;  // next step: the argmax phase advanced it
             }
-            consumer_sync();
+            // a GEMV phase's input planes: one bulk copy issued the moment the
+            // barrier passes (sm.x's readers finished with the previous phase)
+            mbar_wait(&sm.dbar[buf], (gi >> 1) & 1u);
+            const MkPhase& nx = sm.desc[buf];
+            if (nx.kind == kMkGemv) {
+                const uint32_t xbytes = static_cast<uint32_t>(B) * nx.g.in.len * PlaneIO<W>::kBytesPerElem;
+                fence_proxy_async_global();
+                mbar_expect_tx(sm.xbar, xbytes);
+                bulk_g2s_plain(sm.x, nx.g.in.p, xbytes, sm.xbar);
+            }
         }
+        consumer_sync();
         if (tid == 0 && gi + 1 < ntot) {  // prefetch the next descriptor (its buffer's readers are done)
             asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
             mbar_expect_tx(&sm.dbar[buf ^ 1], kDescBytes);
