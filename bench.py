@@ -318,17 +318,18 @@ def run_ours(args):
         L_ = fsvd.lib()
         ip = ctypes.POINTER(ctypes.c_int32)
         fp = ctypes.POINTER(ctypes.c_float)
+        logits_np, tok_np = logits.numpy(), tok.numpy()  # views of the pinned buffers (host argmax in numpy)
         e2e_dec = []
         Ge = min(G, 256)  # host-API decode steps timed per repetition (the whole horizon up to 256)
         for rep in range(max(1, min(args.steps, 2)) + 1):
             sess.reset()
             fsvd._check(L_.fsvd_prefill(sess._h, ctypes.cast(hp.data_ptr(), ip), P, ctypes.cast(logits.data_ptr(), fp)))
-            tok.copy_(logits.argmax(dim=1).to(torch.int32))
+            tok_np[:] = logits_np.argmax(axis=1)
             t0 = time.perf_counter()
             for _ in range(Ge):
                 fsvd._check(L_.fsvd_decode_step(sess._h, ctypes.cast(tok.data_ptr(), ip),
                                                 ctypes.cast(logits.data_ptr(), fp)))
-                tok.copy_(logits.argmax(dim=1).to(torch.int32))
+                tok_np[:] = logits_np.argmax(axis=1)
             if rep > 0:
                 e2e_dec.append(time.perf_counter() - t0)
         e2e_s = max_over_ranks(pg, sum(e2e_dec) / len(e2e_dec))
