@@ -158,7 +158,7 @@ struct MkLaunch {
 };
 
 #ifndef FSVD_MK_CHUNK_LINES
-#define FSVD_MK_CHUNK_LINES 8
+#define FSVD_MK_CHUNK_LINES 12
 #endif
 constexpr int kChunkLines = FSVD_MK_CHUNK_LINES;          // ring chunk: <= 8 lines of one tile
 constexpr int kChunkBytes = kChunkLines * kLineTileBytes;  // 16 KiB
