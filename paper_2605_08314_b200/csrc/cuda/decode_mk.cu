@@ -9,7 +9,7 @@
 //
 //  * Producer warp (one per CTA): walks the GEMV phases of the launch in
 //    order and streams this CTA's weight units through a shared-memory ring
-//    of 24 KiB chunks with cp.async.bulk (mbarrier complete_tx), gated only
+//    of 22 KiB chunks with cp.async.bulk (mbarrier complete_tx), gated only
 //    by free ring slots -- across phase boundaries, so the next phase's
 //    weights land while the consumers wait at the grid barrier.
 //  * Consumer warps (8): per GEMV phase, one bulk copy stages the input

@@ -158,10 +158,10 @@ struct MkLaunch {
 };
 
 #ifndef FSVD_MK_CHUNK_LINES
-#define FSVD_MK_CHUNK_LINES 12  // swept 4-15 on B200: 12 lines x 7 stages is the best trade of per-chunk cost vs ring depth
+#define FSVD_MK_CHUNK_LINES 11  // swept 4-15 on B200: 11 lines x 7 stages is the best trade of per-chunk cost vs ring depth
 #endif
 constexpr int kChunkLines = FSVD_MK_CHUNK_LINES;          // ring chunk: <= kChunkLines lines of one tile (<= 15: 4-bit field)
-constexpr int kChunkBytes = kChunkLines * kLineTileBytes;  // 24 KiB
+constexpr int kChunkBytes = kChunkLines * kLineTileBytes;  // 22 KiB
 constexpr int kMkMaxStages = 32;                           // ring slots (bounded by shared memory)
 
 // ---- host mirrors of the device work split ----
