@@ -15,9 +15,15 @@ device, no host sync), all inputs resident in HBM. value = decode tokens/s
 are reported beside it. Weights (8.3 GB) exceed L2 (126 MB), so no explicit
 L2 flush is needed between steps.
 
-Multi-GPU (torchrun): requests are independent and weights are replicated, so
-each rank runs its own replica ("scaling": "weak"); NCCL is used only for the
-start barrier and the max-over-ranks timing reduction.
+Multi-GPU: `--gpus N` (N > 1) re-launches itself under torch.distributed.run
+(one process per GPU, NCCL, 127.0.0.1) unless already launched that way.
+Requests are independent and weights are replicated, so each rank runs its own
+C2 replica ("scaling": "weak"); NCCL is used only for the start barrier, the
+max-over-ranks timing reduction and the result gather. The C5 leg (BASELINE.json
+configs[4]) is a strong-scaling serving job: 256 requests x (prompt 1024 + 256
+greedy tokens), family B, sharded over the ranks (replicas.shard) in waves of 32,
+tokens all-gathered and digested (c5_tok_s, c5_frac, c5_token_digest: equal at
+every N).
 """
 from __future__ import annotations
 
@@ -65,6 +71,9 @@ def parse():
     p.add_argument("--plan", default="full_step", choices=["eager", "per_layer", "full_step"])
     p.add_argument("--no-cpu-baseline", action="store_true")
     p.add_argument("--cpu-steps", type=int, default=6, help="decode steps in the bounded CPU sample")
+    p.add_argument("--no-c5", action="store_true", help="skip the C5 strong-scaling serving leg")
+    p.add_argument("--c5-requests", type=int, default=256)
+    p.add_argument("--c5-wave", type=int, default=32)
     a = p.parse_args()
     c = CONFIGS[a.config]
     a.prompt = c["prompt"] if a.prompt is None else a.prompt
@@ -83,6 +92,32 @@ def peaks():
         return float(j["hbm_gbs"]), float(j["bf16_tflops"]), float(j.get("bf16_tflops_sustained", j["bf16_tflops"])), "measured"
     except Exception:
         return 6650.0, 1590.0, 1400.0, "fallback"
+
+
+def host_info() -> dict:
+    model = "unknown"
+    try:
+        for line in Path("/proc/cpuinfo").read_text().splitlines():
+            if line.startswith("model name"):
+                model = line.split(":", 1)[1].strip()
+                break
+    except OSError:
+        pass
+    return {"cpu": model, "nproc": os.cpu_count() or 1}
+
+
+def relaunch_distributed(args) -> None:
+    """`--gpus N` without a torchrun environment: re-exec this script as N
+    ranks (one process per GPU) under torch.distributed.run on 127.0.0.1."""
+    import socket
+
+    sk = socket.socket()
+    sk.bind(("127.0.0.1", 0))
+    port = sk.getsockname()[1]
+    sk.close()
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
+           "--master-addr", "127.0.0.1", "--master-port", str(port), str(Path(__file__).resolve()), *sys.argv[1:]]
+    os.execv(sys.executable, cmd)
 
 
 class Clocks:
@@ -214,24 +249,70 @@ def cpu_sample(spec, steps: int, threads: int, use_ref: bool):
 
 
 def run_reference(args):
-    world, rank, local, pg = int(os.environ.get("WORLD_SIZE", "1")), int(os.environ.get("RANK", "0")), 0, None
+    """The reference's CPU path on the box's host cores (rank 0 only): the SPEC
+    runtime restated in oracle/ with the reference's own kern::Ops<float> AVX2
+    gemv (oracle/_ref) -- one independent session per core, each prefilled with
+    a 32-token prompt (setup, untimed), then `warmup` untimed and `steps` timed
+    decode steps; one step = one greedy token on every session."""
+    import numpy as np
+
+    import oracle
+
+    rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
         return
     import paper_2605_08314_b200 as fsvd  # only for the shared config/spec dataclasses
 
     spec = spec_c2(fsvd, args.prompt, args.gen)
     cores = os.cpu_count() or 1
-    for _ in range(max(0, min(args.warmup, 1))):
-        pass
-    res = cpu_sample(spec, max(2, args.cpu_steps // 2), cores, use_ref=True)
-    line = {"metric": "decode tok/s, LLaMA-7B-shape SVD rank 0.6", "value": res["value"], "unit": "tok/s",
+    prompt_len = 32
+    oracle.set_threads(cores)
+    om = oracle.OracleModel.synthetic(spec)
+    sessions = [om.session(f64=False, ffn="no_merge", capacity=prompt_len + args.warmup + args.steps + 4)
+                for _ in range(cores)]
+    rng = np.random.default_rng(2)
+    toks = []
+    for s_ in sessions:  # setup: the oracle's row-batched prefill (not timed)
+        toks.append(int(np.argmax(s_.prefill(rng.integers(0, spec.config.vocab, prompt_len, dtype=np.int32)))))
+    kind = "port"
+    if oracle.ref_available():
+        oracle.lib().oracle_set_ref_gemv(oracle.ref().ref_gemv_f32_ptr())
+        kind = "reference"
+    oracle.set_threads(1)
+    step_s = [[0.0] * cores for _ in range(args.warmup + args.steps)]
+
+    def run(i):
+        tok = toks[i]
+        for k in range(args.warmup + args.steps):
+            t0 = time.perf_counter()
+            tok = int(np.argmax(sessions[i].decode_step(tok)))
+            step_s[k][i] = time.perf_counter() - t0
+
+    ths = [threading.Thread(target=run, args=(i,)) for i in range(cores)]
+    t_all = time.perf_counter()
+    for t in ths:
+        t.start()
+    for t in ths:
+        t.join()
+    t_all = time.perf_counter() - t_all
+    timed = [max(step_s[k]) for k in range(args.warmup, args.warmup + args.steps)]  # slowest core per step
+    wall = sum(timed)
+    value = cores * args.steps / wall
+    ms = sorted(1e3 * x for x in timed)
+    sample = (f"{cores} independent f32 sessions (one per core) x (32-token prompt, {args.warmup} warm-up + "
+              f"{args.steps} timed greedy decode steps at context {prompt_len}-{prompt_len + args.warmup + args.steps}), "
+              f"LLaMA-7B-shape family A rho=0.6 (32 layers, V 32000); gemv = "
+              f"{'reference kern::Ops ' + oracle.ref().ref_active_variant().decode() if kind == 'reference' else 'oracle scalar'}")
+    line = {"metric": "decode tok/s, LLaMA-7B-shape SVD rank 0.6", "value": value, "unit": "tok/s",
             "impl": "reference", "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
-            "ms_per_step": 1000.0 / res["value"] * res["cores"], "higher_is_better": True, "scaling": "weak",
-            "vs_baseline": None, "dtype": "f32", "data": "synthetic",
-            "config": {"workload": "C2 llama7b-shape family A rho=0.6, bounded CPU sample", "batch": 1},
-            "cpu_baseline": {"value": res["value"], "unit": "tok/s", "cores": res["cores"], "kind": res["kind"],
-                             "sample": res["sample"]},
-            "e2e": {"value": res["value"], "unit": "tok/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+            "ms_per_step": wall * 1e3 / args.steps,
+            "ms_per_step_p10_p50_p90": [ms[len(ms) // 10], ms[len(ms) // 2], ms[min(len(ms) - 1, len(ms) * 9 // 10)]],
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
+            "config": {"workload": args.workload + " -- reference CPU path, bounded sample", "batch": 1},
+            "host": host_info(),
+            "cpu_baseline": {"value": value, "unit": "tok/s", "cores": cores, "kind": kind, "sample": sample},
+            "e2e": {"value": value, "unit": "tok/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+            "run_seconds": t_all}
     print(json.dumps(line), flush=True)
 
 
@@ -291,6 +372,8 @@ def run_ours(args):
     barrier(pg)
 
     decode_tok_s = world * B * G * args.steps / (dec_total / 1e3)
+    per_tok = sorted(m / G for m in dec_ms)  # per-request decode ms/token (SPEC.md:528 median, p10, p90)
+    pct = [per_tok[len(per_tok) // 10], per_tok[len(per_tok) // 2], per_tok[min(len(per_tok) - 1, len(per_tok) * 9 // 10)]]
     prefill_tok_s = world * B * P * args.steps / (pre_total / 1e3)
     ms_per_token = dec_total / (G * args.steps)
 
@@ -307,35 +390,83 @@ def run_ours(args):
     prefill_tflops = prefill_flops / (pre_total / args.steps / 1e3) / 1e12
 
     # ---- end to end through the host-pointer C ABI (pinned host buffers) ----
-    e2e = None
-    if rank == 0 or True:
-        hp = torch.empty((B, P), dtype=torch.int32, pin_memory=True)
-        hp.copy_(prompts.cpu())
-        tok = torch.zeros((B,), dtype=torch.int32, pin_memory=True)
-        logits = torch.empty((B, cfg.vocab), dtype=torch.float32, pin_memory=True)
-        import ctypes
+    # per request: fsvd_prefill (host prompt in, host logits out) + G x
+    # fsvd_decode_step (host token in, host logits out, host argmax) -- the
+    # SPEC's end-to-end definition (includes prefill)
+    hp = torch.empty((B, P), dtype=torch.int32, pin_memory=True)
+    hp.copy_(prompts.cpu())
+    tok = torch.zeros((B,), dtype=torch.int32, pin_memory=True)
+    logits = torch.empty((B, cfg.vocab), dtype=torch.float32, pin_memory=True)
+    import ctypes
 
-        L_ = fsvd.lib()
-        ip = ctypes.POINTER(ctypes.c_int32)
-        fp = ctypes.POINTER(ctypes.c_float)
-        logits_np, tok_np = logits.numpy(), tok.numpy()  # views of the pinned buffers (host argmax in numpy)
-        e2e_dec = []
-        Ge = min(G, 256)  # host-API decode steps timed per repetition (the whole horizon up to 256)
-        for rep in range(max(1, min(args.steps, 2)) + 1):
-            sess.reset()
-            fsvd._check(L_.fsvd_prefill(sess._h, ctypes.cast(hp.data_ptr(), ip), P, ctypes.cast(logits.data_ptr(), fp)))
+    L_ = fsvd.lib()
+    ip = ctypes.POINTER(ctypes.c_int32)
+    fp = ctypes.POINTER(ctypes.c_float)
+    logits_np, tok_np = logits.numpy(), tok.numpy()  # views of the pinned buffers (host argmax in numpy)
+    e2e_s = []
+    for rep in range(max(1, min(args.steps, 2)) + 1):
+        sess.reset()
+        t0 = time.perf_counter()
+        fsvd._check(L_.fsvd_prefill(sess._h, ctypes.cast(hp.data_ptr(), ip), P, ctypes.cast(logits.data_ptr(), fp)))
+        tok_np[:] = logits_np.argmax(axis=1)
+        for _ in range(G):
+            fsvd._check(L_.fsvd_decode_step(sess._h, ctypes.cast(tok.data_ptr(), ip),
+                                            ctypes.cast(logits.data_ptr(), fp)))
             tok_np[:] = logits_np.argmax(axis=1)
-            t0 = time.perf_counter()
-            for _ in range(Ge):
-                fsvd._check(L_.fsvd_decode_step(sess._h, ctypes.cast(tok.data_ptr(), ip),
-                                                ctypes.cast(logits.data_ptr(), fp)))
-                tok_np[:] = logits_np.argmax(axis=1)
-            if rep > 0:
-                e2e_dec.append(time.perf_counter() - t0)
-        e2e_s = max_over_ranks(pg, sum(e2e_dec) / len(e2e_dec))
-        e2e = {"value": world * B * Ge / e2e_s, "unit": "tok/s",
-               "h2d_bytes_per_step": B * 4 * Ge, "d2h_bytes_per_step": B * cfg.vocab * 4 * Ge,
-               "note": "fsvd_decode_step host API per token (pinned host token in, host logits out, host argmax)"}
+        if rep > 0:
+            e2e_s.append(time.perf_counter() - t0)
+    e2e_req = max_over_ranks(pg, sum(e2e_s) / len(e2e_s))
+    e2e = {"value": world * B * G / e2e_req, "unit": "tok/s",
+           "h2d_bytes_per_step": B * P * 4 + B * 4 * G, "d2h_bytes_per_step": B * cfg.vocab * 4 * (G + 1),
+           "ms_per_request": e2e_req * 1e3,
+           "note": "per request: fsvd_prefill (pinned host prompt in, host logits out) + G x fsvd_decode_step "
+                   "(pinned host token in, host logits out, host argmax); generated tokens / request wall time"}
+    del sess
+    del model
+
+    # ---- C5: strong-scaling serving leg (BASELINE.json configs[4]) ----
+    c5 = None
+    if not args.no_c5 and args.config == "c2":
+        from paper_2605_08314_b200 import replicas
+
+        c5c = CONFIGS["c5"]
+        P5, G5, W5, N5 = c5c["prompt"], c5c["gen"], args.c5_wave, args.c5_requests
+        spec5 = fsvd.SynthSpec(fsvd.PRESETS[c5c["model"]][0], capacity=P5 + G5 + 16, family=c5c["family"], rho=RHO,
+                               seed=SEED)
+        model5 = fsvd.Model.synthetic(spec5, dtype="bf16", device=local)
+        info5 = model5.info()
+        sessions = {}
+
+        def session_for(nb):
+            if nb not in sessions:
+                sessions[nb] = fsvd.Session(model5, batch=nb, capacity=spec5.capacity, plan="full_step")
+            return sessions[nb]
+
+        # warm-up: build the wave-size session (graph capture) and run one short wave
+        mine = replicas.shard(N5, world, rank)
+        for w in replicas.waves(mine, W5)[:1]:
+            sw = session_for(len(w))
+            sw.reset()
+            sw.generate(np.stack([replicas.request_prompt(i, P5, cfg.vocab) for i in w]), 4)
+        toks5, dt5, n_mine = replicas.serve(pg, N5, W5, P5, G5, cfg.vocab, session_for, sync=torch.cuda.synchronize)
+        # roofline time of this rank's share: prefill FLOPs at the bf16 peak + decode bytes at HBM peak
+        ideal = 0.0
+        for w in replicas.waves(mine, W5):
+            nb = len(w)
+            pf = nb * (P5 * 2 * (info5["decode_weight_bytes"] - cfg.vocab * d * 2) / 2 + 2 * L * P5 * P5 * d)
+            ideal += pf / (tf_burst * 1e12)
+            for j in range(G5):
+                ideal += (info5["decode_weight_bytes"] + nb * ((P5 + j + 1) * L * 2 * d * 2)) / (hbm * 1e9)
+        ideal = max_over_ranks(pg, ideal)
+        c5 = {"workload": c5c["desc"].replace("waves of 32", f"waves of {W5}"), "requests": N5,
+              "c5_tok_s": N5 * G5 / dt5, "c5_seconds": dt5, "c5_frac": ideal / dt5,
+              "c5_frac_def": "roofline time (prefill FLOPs / bf16 peak + decode bytes / HBM peak, this rank's waves) "
+                             "/ measured wall time, max over ranks",
+              "c5_token_digest": replicas.token_digest(toks5), "c5_tokens_gathered": list(toks5.shape),
+              "timing": "host wall clock (perf_counter) around the rank's serving loop, torch.cuda.synchronize "
+                        "on both sides, max over ranks"}
+        del sessions
+        del model5
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
@@ -365,6 +496,7 @@ def run_ours(args):
                        "l2": "weights 8.3 GB > 126 MB L2: no flush needed"},
             "engine": engine,
             "decode_ms_per_token": ms_per_token,
+            "decode_ms_per_token_p10_p50_p90": pct,
             "prefill_tok_s": prefill_tok_s,
             "prefill_ms": pre_total / args.steps,
             "prefill_tflops": prefill_tflops,
@@ -376,7 +508,10 @@ def run_ours(args):
             "gpu_launches": None,
             "clocks": clk.summary(),
             "cpu_baseline": cpu,
+            "host": host_info(),
         }
+        if c5:
+            line.update(c5)
         # our kernels in the timed region, per request: prefill = embed + per layer (2 RMSNorm,
         # 8 tcgen05 GEMMs, 1 flash attention, 2 split-K reductions at prompt 512) + gather + 2
         # length-register sets + the head/argmax megakernel; decode = one full-step megakernel
@@ -406,6 +541,11 @@ def run_ours(args):
 
 def main():
     args = parse()
+    world = os.environ.get("WORLD_SIZE")
+    if world is None and args.gpus > 1:
+        relaunch_distributed(args)  # does not return
+    if world is not None and int(world) != args.gpus:
+        raise SystemExit(f"bench.py: --gpus {args.gpus} but WORLD_SIZE={world}")
     if args.impl == "reference":
         run_reference(args)
     else:

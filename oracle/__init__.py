@@ -47,6 +47,7 @@ def lib() -> C.CDLL:
             "oracle_tensor": ([vp, C.c_char_p, C.POINTER(C.c_float), u64], C.c_int),
             "oracle_session": ([vp, C.c_int, C.c_int, u64], vp),
             "oracle_free_session": ([vp], None),
+            "oracle_clone_session": ([vp], vp),
             "oracle_prefill": ([vp, i32p, u64, dp], C.c_int),
             "oracle_decode": ([vp, C.c_int32, dp], C.c_int),
             "oracle_generate": ([vp, i32p, u64, u64, i32p], C.c_int),
@@ -187,9 +188,13 @@ class OracleModel:
 
 
 class OracleSession:
-    def __init__(self, model: OracleModel, f64: bool, ffn: str, capacity: int):
+    def __init__(self, model: OracleModel, f64: bool, ffn: str, capacity: int, _handle=None):
         self.model = model
-        self._h = lib().oracle_session(model._h, 1 if f64 else 0, 2 if ffn == "packed" else 1, capacity)
+        self._h = _handle or lib().oracle_session(model._h, 1 if f64 else 0, 2 if ffn == "packed" else 1, capacity)
+
+    def clone(self) -> "OracleSession":
+        """Independent copy (KV cache + position): fork a shared prompt prefix."""
+        return OracleSession(self.model, True, "", 0, _handle=lib().oracle_clone_session(self._h))
 
     def prefill(self, tokens):
         t = np.ascontiguousarray(np.asarray(tokens, dtype=np.int32))

@@ -150,6 +150,52 @@ void gemv_any(T* y, const T* x, const Mat& A) {
         gemv<T>(y, x, A);
 }
 
+// Y[t] = X[t] . A for n rows: the same per-(t, column) accumulation as gemv
+// (k in index order from zero), rows blocked 8 at a time so each weight row is
+// read once per block instead of once per token -- bitwise identical to n
+// gemv calls (tensor.hpp:100-119: matmul == triple loop). Used by the prefill
+// restatement, where the oracle is otherwise weight-stream
+// bound. With the reference gemv plugged in (CPU baseline), rows go through it.
+template <typename T>
+void gemv_rows(size_t n, const T* const* X, T* const* Y, const Mat& A) {
+    if constexpr (std::is_same_v<T, float>)
+        if (g_ref_gemv) {
+            for (size_t t = 0; t < n; ++t) gemv_f32(Y[t], X[t], A);
+            return;
+        }
+    const size_t m = A.rows, nc = A.cols;
+    constexpr size_t RB = 8;
+    parallel_cols(nc, [&](size_t lo, size_t hi) {
+        for (size_t t0 = 0; t0 < n; t0 += RB) {
+            const size_t t1 = std::min(n, t0 + RB);
+            for (size_t t = t0; t < t1; ++t)
+                for (size_t j = lo; j < hi; ++j) Y[t][j] = T(0);
+            for (size_t k = 0; k < m; ++k) {
+                const float* row = A.v.data() + k * nc;
+                for (size_t t = t0; t < t1; ++t) {
+                    const T xk = X[t][k];
+                    T* y = Y[t];
+                    for (size_t j = lo; j < hi; ++j) y[j] += xk * static_cast<T>(row[j]);
+                }
+            }
+        }
+    });
+}
+
+template <typename T>
+struct Rows {  // n row vectors of one width, with pointer tables for gemv_rows
+    std::vector<std::vector<T>> r;
+    std::vector<T*> p;
+    Rows(size_t n, size_t w) : r(n, std::vector<T>(w)), p(n) {
+        for (size_t i = 0; i < n; ++i) p[i] = r[i].data();
+    }
+    std::vector<const T*> cp(size_t off = 0) const {
+        std::vector<const T*> q(r.size());
+        for (size_t i = 0; i < r.size(); ++i) q[i] = r[i].data() + off;
+        return q;
+    }
+};
+
 template <typename T>
 T dot(const T* a, const T* b, size_t n) {  // kernels_scalar.cpp:23-28
     T s = T(0);
@@ -603,65 +649,90 @@ struct Session {
     // P = X.A once for the prompt; K/V reconstructed and
     // RoPE'd in blocks of 64 and written to the cache; causal online softmax
     // over 64-key blocks.
+    // FFN of n rows at once (ffn_apply row by row, bitwise: gemv_rows)
+    void ffn_rows(const Layer& L, const Rows<T>& xn, Rows<T>& out) {
+        const Config& c = m->c;
+        const size_t n = xn.r.size();
+        Rows<T> u(n, c.dff), g(n, c.dff), h(n, c.dff);
+        const auto xp = xn.cp();
+        if (ffn == 2) {
+            Rows<T> p(n, L.a_ug.cols);
+            gemv_rows<T>(n, xp.data(), p.p.data(), L.a_ug);
+            gemv_rows<T>(n, p.cp().data(), u.p.data(), *L.p[4].b);
+            gemv_rows<T>(n, p.cp(L.r_up).data(), g.p.data(), *L.p[5].b);
+        } else {
+            Rows<T> pu(n, L.p[4].rank), pg(n, L.p[5].rank);
+            gemv_rows<T>(n, xp.data(), pu.p.data(), *L.p[4].a);
+            gemv_rows<T>(n, pu.cp().data(), u.p.data(), *L.p[4].b);
+            gemv_rows<T>(n, xp.data(), pg.p.data(), *L.p[5].a);
+            gemv_rows<T>(n, pg.cp().data(), g.p.data(), *L.p[5].b);
+        }
+        for (size_t t = 0; t < n; ++t) silu_mul<T>(h.p[t], g.p[t], u.p[t], c.dff);
+        Rows<T> pd(n, L.p[6].rank);
+        gemv_rows<T>(n, h.cp().data(), pd.p.data(), *L.p[6].a);
+        gemv_rows<T>(n, pd.cp().data(), out.p.data(), *L.p[6].b);
+    }
+
+    // P = X.A once for the prompt; K/V reconstructed and
+    // RoPE'd (the SPEC's 64-row blocks; rows are independent, so the blocking
+    // does not change any value) and written to the cache; causal online
+    // softmax over 64-key blocks. Row-batched (gemv_rows): bitwise the same as
+    // token-by-token gemv.
     void prefill(const int* tok, size_t T_, T* logits) {
         const Config& c = m->c;
         if (T_ == 0) throw std::runtime_error("shape");
         if (pos + T_ > cap) throw std::runtime_error("capacity");
         const size_t p0 = pos, blk = 64;
-        std::vector<std::vector<T>> X(T_, std::vector<T>(c.d));
+        Rows<T> X(T_, c.d);
         for (size_t t = 0; t < T_; ++t)
-            for (size_t i = 0; i < c.d; ++i) X[t][i] = static_cast<T>(m->emb.at(static_cast<size_t>(tok[t]), i));
+            for (size_t i = 0; i < c.d; ++i) X.r[t][i] = static_cast<T>(m->emb.at(static_cast<size_t>(tok[t]), i));
         const T scale = static_cast<T>(1.0 / std::sqrt(static_cast<double>(c.dh)));
-        std::vector<T> xn(c.d), row(c.d), tmp;
+        Rows<T> XN(T_, c.d), Q(T_, c.d), Kr(T_, c.d), Vr(T_, c.d), A(T_, c.d), O(T_, c.d);
         for (size_t l = 0; l < c.L; ++l) {
             const Layer& L = m->layers[l];
-            std::vector<std::vector<T>> Pq(T_), Pk(T_), Pv(T_);
-            for (size_t t = 0; t < T_; ++t) {
-                rmsnorm<T>(xn.data(), X[t].data(), L.attn_gamma, c.d, static_cast<T>(c.eps));
-                Pq[t].resize(L.p[0].rank);
-                Pk[t].resize(L.p[1].rank);
-                Pv[t].resize(L.p[2].rank);
-                gemv_any<T>(Pq[t].data(), xn.data(), *L.p[0].a);
-                gemv_any<T>(Pk[t].data(), xn.data(), *L.p[1].a);
-                gemv_any<T>(Pv[t].data(), xn.data(), *L.p[2].a);
+            for (size_t t = 0; t < T_; ++t)
+                rmsnorm<T>(XN.p[t], X.p[t], L.attn_gamma, c.d, static_cast<T>(c.eps));
+            const auto xn = XN.cp();
+            Rows<T>* outs[3] = {&Q, &Kr, &Vr};
+            for (int j = 0; j < 3; ++j) {
+                Rows<T> P(T_, L.p[j].rank);
+                gemv_rows<T>(T_, xn.data(), P.p.data(), *L.p[j].a);
+                gemv_rows<T>(T_, P.cp().data(), outs[j]->p.data(), *L.p[j].b);
             }
-            // blockwise K/V reconstruction + RoPE into the dense cache
-            std::vector<std::vector<T>> Q(T_, std::vector<T>(c.d));
-            for (size_t b0 = 0; b0 < T_; b0 += blk)
-                for (size_t t = b0; t < std::min(T_, b0 + blk); ++t) {
-                    const double ps = static_cast<double>(p0 + t);
-                    gemv_any<T>(Q[t].data(), Pq[t].data(), *L.p[0].b);
-                    gemv_any<T>(row.data(), Pk[t].data(), *L.p[1].b);
-                    for (size_t h = 0; h < c.H; ++h) {
-                        rope<T>(Q[t].data() + h * c.dh, c.dh, ps, c.rope_base);
-                        rope<T>(row.data() + h * c.dh, c.dh, ps, c.rope_base);
-                        std::copy(row.begin() + h * c.dh, row.begin() + (h + 1) * c.dh, krow(l, h, p0 + t));
-                    }
-                    gemv_any<T>(row.data(), Pv[t].data(), *L.p[2].b);
-                    for (size_t h = 0; h < c.H; ++h)
-                        std::copy(row.begin() + h * c.dh, row.begin() + (h + 1) * c.dh, vrow(l, h, p0 + t));
+            for (size_t t = 0; t < T_; ++t) {
+                const double ps = static_cast<double>(p0 + t);
+                for (size_t h = 0; h < c.H; ++h) {
+                    rope<T>(Q.p[t] + h * c.dh, c.dh, ps, c.rope_base);
+                    rope<T>(Kr.p[t] + h * c.dh, c.dh, ps, c.rope_base);
+                    std::copy(Kr.p[t] + h * c.dh, Kr.p[t] + (h + 1) * c.dh, krow(l, h, p0 + t));
+                    std::copy(Vr.p[t] + h * c.dh, Vr.p[t] + (h + 1) * c.dh, vrow(l, h, p0 + t));
                 }
-            std::vector<T> att(c.d), o(c.d);
+            }
             Online<T> st;
             for (size_t t = 0; t < T_; ++t) {
                 const size_t nk = p0 + t + 1;
                 for (size_t h = 0; h < c.H; ++h) {
                     st.reset(c.dh);
                     for (size_t k0 = 0; k0 < nk; k0 += blk)
-                        st.update(Q[t].data() + h * c.dh, krow(l, h, k0), vrow(l, h, k0), std::min(blk, nk - k0),
-                                  c.dh, c.dh, scale);
-                    st.finish(att.data() + h * c.dh, c.dh);
+                        st.update(Q.p[t] + h * c.dh, krow(l, h, k0), vrow(l, h, k0), std::min(blk, nk - k0), c.dh,
+                                  c.dh, scale);
+                    st.finish(A.p[t] + h * c.dh, c.dh);
                 }
-                lowrank<T>(o.data(), att.data(), L.p[3], tmp);
-                for (size_t i = 0; i < c.d; ++i) X[t][i] += o[i];
             }
-            for (size_t t = 0; t < T_; ++t) {
-                rmsnorm<T>(xn.data(), X[t].data(), L.mlp_gamma, c.d, static_cast<T>(c.eps));
-                ffn_apply(L, xn.data(), o.data());
-                for (size_t i = 0; i < c.d; ++i) X[t][i] += o[i];
+            {
+                Rows<T> P(T_, L.p[3].rank);
+                gemv_rows<T>(T_, A.cp().data(), P.p.data(), *L.p[3].a);
+                gemv_rows<T>(T_, P.cp().data(), O.p.data(), *L.p[3].b);
             }
+            for (size_t t = 0; t < T_; ++t)
+                for (size_t i = 0; i < c.d; ++i) X.r[t][i] += O.r[t][i];
+            for (size_t t = 0; t < T_; ++t)
+                rmsnorm<T>(XN.p[t], X.p[t], L.mlp_gamma, c.d, static_cast<T>(c.eps));
+            ffn_rows(L, XN, O);
+            for (size_t t = 0; t < T_; ++t)
+                for (size_t i = 0; i < c.d; ++i) X.r[t][i] += O.r[t][i];
         }
-        head(X[T_ - 1].data(), logits);
+        head(X.p[T_ - 1], logits);
         pos = p0 + T_;
     }
 };
@@ -826,6 +897,15 @@ void* oracle_session(void* mp, int f64, int ffn, uint64_t cap) {
     return s;
 }
 void oracle_free_session(void* s) { delete static_cast<Sess*>(s); }
+// Independent copy of a session (KV cache and position): forks one prompt
+// prefix into several continuations without recomputing it (tests only).
+void* oracle_clone_session(void* sp) {
+    const Sess& s = *static_cast<Sess*>(sp);
+    auto* c = new Sess();
+    if (s.d) c->d = std::make_unique<Session<double>>(*s.d);
+    if (s.f) c->f = std::make_unique<Session<float>>(*s.f);
+    return c;
+}
 
 int oracle_prefill(void* sp, const int32_t* tok, uint64_t T, double* logits) {
     return wrap([&] {

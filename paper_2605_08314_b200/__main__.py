@@ -90,7 +90,10 @@ def main(argv=None) -> int:
         p.add_argument("--plan", default="full_step", choices=["eager", "per_layer", "full_step"])
         p.add_argument("--runs", type=int, default=3)
         p.add_argument("--prompts", type=int, default=20)
-        p.add_argument("--gold", help="audit: .npy [prompts][gen] gold greedy tokens")
+        p.add_argument("--gold", help="audit: .npy [prompts][gen] f64 no-cache gold greedy tokens "
+                                      "(tools/audit_fidelity.py writes them from the CPU oracle)")
+        p.add_argument("--pairwise-only", action="store_true",
+                       help="audit without gold: report only eager vs per_layer agreement")
         p.add_argument("--json")
     try:
         a = ap.parse_args(argv)
@@ -130,9 +133,17 @@ def main(argv=None) -> int:
             prompts = audit_prompts(a.prompts, vocab, seed=a.seed + 1)
             eager = generate_candidates(model, prompts, a.gen, plan="eager")
             layer = generate_candidates(model, prompts, a.gen, plan="per_layer")
-            gold = list(np.load(a.gold)) if a.gold else eager
-            out = score(gold, eager, layer).as_dict()
-            out["gold"] = a.gold or "eager candidate (pairwise only)"
+            if a.gold:
+                gold = list(np.load(a.gold))
+                out = score(gold, eager, layer).as_dict()
+                out["gold"] = a.gold
+            elif a.pairwise_only:
+                out = {"n_prompts": len(prompts), "max_new": a.gen,
+                       "pairwise_exact": sum(int(np.array_equal(x, y)) for x, y in zip(eager, layer)),
+                       "gold": None}
+            else:
+                raise ValueError("audit: --gold <f64 gold tokens .npy> is required (SPEC.md:503-511 scores against "
+                                 "the f64 no-cache gold; tools/audit_fidelity.py produces it), or pass --pairwise-only")
             print(json.dumps(out))
         if a.json:
             with open(a.json, "w") as f:

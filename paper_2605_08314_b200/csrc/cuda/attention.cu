@@ -1,8 +1,9 @@
 // Prefill causal attention: a T-token chunk at positions
 // [p0, p0+T) attends cache rows [0, p0+T). Blockwise online softmax
 // (partition-invariant; math.hpp:56-101) with 64-key tiles
-// staged in shared memory. Decode attention lives in the megakernel
-// (decode_mk_attn.cuh).
+// staged in shared memory. Batch-1/2 decode attention runs inside the decode
+// megakernel (decode_mk.cu, attn_phase); the batched engine's split-KV flash
+// decode is attn_decode_kernel below.
 #include <math_constants.h>
 
 #include <algorithm>

@@ -6,10 +6,10 @@
 //
 // One CTA per 128 x BN output tile, warp-specialized:
 //   warp 0      TMA producer: X tile (128 tokens x 64 k, SWIZZLE_128B) via a
-//               tensor map (cp.async.bulk.tensor.2d), W^T tile via BN/16
-//               contiguous 2 KiB cp.async.bulk copies -- the device weight
-//               layout (layout.h) already IS the K-major SWIZZLE_128B
-//               core-matrix image, so weights land in shared memory verbatim;
+//               tensor map (cp.async.bulk.tensor.2d), W^T tile as ONE 4-D
+//               tensor-map box {64 el, 16 rows, line, BN/16 tiles} over the
+//               device weight layout (layout.h), which already IS the K-major
+//               SWIZZLE_128B core-matrix image, so weights land verbatim;
 //   warp 1      MMA issuer: one elected thread issues tcgen05.mma
 //               (kind::f16, M=128, N=BN, K=16) into a TMEM fp32 accumulator
 //               and tcgen05.commit's each stage back to the producer;

@@ -97,3 +97,60 @@ def gather_rows(pg, rows, n_total: int):
     pg.all_gather(out, buf)
     parts = [out[r][: len(shard(n_total, world, r))] for r in range(world)]
     return torch.cat(parts).cpu()
+
+
+def token_digest(tokens) -> str:
+    """Order-sensitive digest of a [requests, gen] int32 token table (sha256 of
+    the little-endian bytes, first 16 hex digits): equal digests at N = 1 and
+    N > 1 mean every request produced the same tokens on every rank layout."""
+    import hashlib
+
+    import numpy as np
+
+    a = np.ascontiguousarray(np.asarray(tokens, dtype="<i4"))
+    return hashlib.sha256(a.tobytes()).hexdigest()[:16]
+
+
+def request_prompt(i: int, prompt_len: int, vocab: int):
+    """Prompt of request i: seeded per request (seed 2 + i)."""
+    import numpy as np
+
+    return np.random.default_rng(2 + i).integers(0, vocab, prompt_len, dtype=np.int32)
+
+
+def serve(pg, n_requests: int, per_wave: int, prompt_len: int, gen: int, vocab: int, session_for, sync=None):
+    """C5 serving job (BASELINE.json configs[4]): this rank's
+    contiguous share of n_requests, in waves of <= per_wave, each wave one
+    batched prefill + `gen` greedy steps through `session_for(B).generate`;
+    then the generated tokens of every rank are all-gathered (rank order).
+
+    Returns (tokens [n_requests, gen] on every rank, seconds = max over ranks
+    of this rank's wall time, requests served by this rank). `sync()` (e.g.
+    torch.cuda.synchronize) brackets the timed region. No collective runs
+    inside it: the requests are independent and the weights replicated."""
+    import time
+
+    import numpy as np
+    import torch
+
+    world = pg.get_world_size() if pg is not None else 1
+    rank = pg.get_rank() if pg is not None else 0
+    mine = shard(n_requests, world, rank)
+    toks = np.zeros((len(mine), gen), dtype=np.int32)
+    prompts = {i: request_prompt(i, prompt_len, vocab) for i in mine}
+    barrier(pg)
+    if sync:
+        sync()
+    t0 = time.perf_counter()
+    row = 0
+    for w in waves(mine, per_wave):
+        s = session_for(len(w))
+        s.reset()
+        out = s.generate(np.stack([prompts[i] for i in w]), gen)
+        toks[row: row + len(w)] = out
+        row += len(w)
+    if sync:
+        sync()
+    dt = max_over_ranks(pg, time.perf_counter() - t0)
+    allt = gather_rows(pg, torch.from_numpy(toks), n_requests)
+    return np.asarray(allt), dt, len(mine)
