@@ -44,7 +44,8 @@ def json_include_dir() -> Path:
     raise RuntimeError("nlohmann json.hpp not found (needed by the FSVD15 header parser)")
 
 
-HOST_SOURCES = ["host/model.cpp", "host/checkpoint.cpp", "host/canonical.cpp", "host/synth.cpp", "capi/capi.cpp"]
+HOST_SOURCES = ["host/model.cpp", "host/checkpoint.cpp", "host/canonical.cpp", "host/synth.cpp", "host/cpu_kernels.cpp",
+                "capi/capi.cpp"]
 CUDA_SOURCES = [
     "cuda/decode_mk.cu",
     "cuda/attention.cu",

@@ -392,7 +392,21 @@ k::GemvSeg Session::seg(const DeviceMatrix& mtx, int x_off, int y_off, int epi) 
     return k::GemvSeg{mtx.w, mtx.rows, mtx.k, mtx.kp, x_off, y_off, epi};
 }
 
+// A constructor that throws never runs ~Session: free whatever init() had
+// allocated (device buffers, stream, graphs) before rethrowing, so a caller
+// retrying with another shape does not leak HBM (ConfigError from the
+// megakernel's shared-memory sizing happens after the KV cache allocation).
 Session::Session(DeviceModel* m, const fsvd_session_opts& o) : m_(m) {
+    try {
+        init(o);
+    } catch (...) {
+        release();
+        throw;
+    }
+}
+
+void Session::init(const fsvd_session_opts& o) {
+    DeviceModel* m = m_;
     const ModelConfig& c = m->cfg;
     B_ = static_cast<int>(o.batch);
     if (B_ < 1) throw ConfigError("session batch must be >= 1");
@@ -469,14 +483,21 @@ Session::Session(DeviceModel* m, const fsvd_session_opts& o) : m_(m) {
     stats_.allocs = 0;
 }
 
-Session::~Session() {
+Session::~Session() { release(); }
+
+void Session::release() {
     cudaSetDevice(m_->device);
     if (stream_) cudaStreamSynchronize(stream_);
     for (auto g : layer_graphs_) cudaGraphExecDestroy(g);
+    layer_graphs_.clear();
     if (step_graph_) cudaGraphExecDestroy(step_graph_);
+    step_graph_ = nullptr;
     if (bstep_graph_) cudaGraphExecDestroy(bstep_graph_);
+    bstep_graph_ = nullptr;
     for (void* p : allocations_) cudaFree(p);
+    allocations_.clear();
     if (stream_) cudaStreamDestroy(stream_);
+    stream_ = nullptr;
 }
 
 void* Session::staging(size_t bytes) {

@@ -120,6 +120,8 @@ class Session {
     bool batched() const { return batched_; }
 
   private:
+    void init(const fsvd_session_opts& o);
+    void release();  // frees every device resource; safe on a partly built session
     void build_program();
     void add_layer_phases(size_t l, const float* next_gamma);
     void mk_run(int p_begin, int p_end, int reps = 1);

@@ -60,3 +60,19 @@ def test_cpp_wrapper_rethrows_reference_exceptions(fsvd, tmp_path):
     subprocess.run(cmd, check=True, capture_output=True, text=True)
     r = subprocess.run([str(exe)], capture_output=True, text=True)
     assert r.returncode == 0 and "OK" in r.stdout, r.stdout + r.stderr
+
+
+def test_cpu_operator_api_matches_reference_golden(fsvd, tmp_path):
+    """include/fsvd/kernels.hpp + math.hpp (the reference's kern::Ops registry
+    and math layer, kernels.hpp:18-62 / math.hpp:16-140) compile against this
+    tree, link to libfsvd_b200.so, and reproduce the reference's own scalar
+    outputs bit for bit (tests/golden/primitives.json)."""
+    from paper_2605_08314_b200.build import json_include_dir
+
+    exe = tmp_path / "cpu_ops_check"
+    cmd = ["g++", "-std=c++20", "-O2", "-ffp-contract=off", "-I", str(ROOT / "include"), "-I", str(json_include_dir()),
+           str(ROOT / "tests/cpp/cpu_ops_check.cpp"), "-o", str(exe), "-L", str(fsvd.LIB_PATH.parent), "-lfsvd_b200",
+           f"-Wl,-rpath,{fsvd.LIB_PATH.parent}"]
+    subprocess.run(cmd, check=True, capture_output=True, text=True)
+    r = subprocess.run([str(exe), str(ROOT / "tests/golden/primitives.json")], capture_output=True, text=True)
+    assert r.returncode == 0 and "OK" in r.stdout, r.stdout + r.stderr

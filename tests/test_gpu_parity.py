@@ -272,3 +272,22 @@ def test_llama7b_shape_two_layers_vs_oracle(fsvd, oracle_mod, batch):
             tok = int(np.argmax(got[i + 1][b]))
         errs = [oracle_mod.rel_err(got[i][b], want[i]) for i in range(3)]
         assert max(errs) <= TOL["bf16"], (b, errs)
+
+
+def test_failed_session_create_frees_its_allocations(fsvd):
+    """A session whose construction fails after allocating the KV cache (the
+    megakernel's shared memory does not fit this batch x d_ff) raises
+    ConfigError and frees everything (no HBM leak across retries)."""
+    import torch
+
+    cfg = fsvd.ModelConfig(2, 128, 4, 32, 32768, 512)  # B=2 x d_ff 32768 planes exceed shared memory
+    spec = _spec(fsvd, "A", cfg=cfg, cap=32768)
+    model = fsvd.Model.synthetic(spec, dtype="f32")
+    torch.cuda.synchronize()
+    free0 = torch.cuda.mem_get_info()[0]
+    for _ in range(10):
+        with pytest.raises(fsvd.ConfigError):
+            fsvd.Session(model, batch=2, capacity=32768, plan="full_step")
+    torch.cuda.synchronize()
+    free1 = torch.cuda.mem_get_info()[0]
+    assert free0 - free1 < 64 << 20, (free0 - free1) / 2**20
