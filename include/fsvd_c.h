@@ -122,6 +122,9 @@ fsvd_status fsvd_synthetic_write_file(const fsvd_synth_spec* spec, const char* p
 
 /* ---- device model ---- */
 fsvd_status fsvd_model_load(const char* path, fsvd_dtype dtype, int32_t device, fsvd_model** out);
+/* Statistics of this thread's last fsvd_model_load (streaming loader): wall
+ * seconds, payload bytes read, host pinned staging held at once. */
+fsvd_status fsvd_last_load_stats(double* seconds, uint64_t* payload_bytes, uint64_t* pinned_bytes);
 fsvd_status fsvd_model_from_canonical(const fsvd_canonical* c, fsvd_dtype dtype, int32_t device, fsvd_model** out);
 /* Device-side generation of a synthetic checkpoint: bit-identical weights to
  * fsvd_canonical_synthetic(spec) without a host copy (LLaMA-13B shape). */

@@ -181,6 +181,7 @@ def lib() -> C.CDLL:
         "fsvd_canonical_destroy": ([vp], C.c_int),
         "fsvd_synthetic_write_file": ([C.POINTER(_Synth), C.c_char_p], C.c_int),
         "fsvd_model_load": ([C.c_char_p, C.c_int, i32, C.POINTER(vp)], C.c_int),
+        "fsvd_last_load_stats": ([C.POINTER(C.c_double), C.POINTER(C.c_uint64), C.POINTER(C.c_uint64)], C.c_int),
         "fsvd_model_from_canonical": ([vp, C.c_int, i32, C.POINTER(vp)], C.c_int),
         "fsvd_model_synthetic": ([C.POINTER(_Synth), C.c_int, i32, C.POINTER(vp)], C.c_int),
         "fsvd_model_info": ([vp, C.POINTER(_Config), C.POINTER(u64), C.POINTER(u64), C.POINTER(u64)], C.c_int),
@@ -218,7 +219,8 @@ def exported_symbols() -> list[str]:
     return ["fsvd_last_error", "fsvd_version", "fsvd_canonical_load_file", "fsvd_canonical_load_bytes",
             "fsvd_canonical_synthetic", "fsvd_canonical_config", "fsvd_canonical_rank", "fsvd_canonical_copy",
             "fsvd_canonical_shared_count", "fsvd_canonical_aliased", "fsvd_canonical_destroy",
-            "fsvd_synthetic_write_file", "fsvd_model_load", "fsvd_model_from_canonical", "fsvd_model_synthetic",
+            "fsvd_synthetic_write_file", "fsvd_model_load", "fsvd_last_load_stats", "fsvd_model_from_canonical",
+            "fsvd_model_synthetic",
             "fsvd_model_info", "fsvd_model_copy_factor", "fsvd_model_destroy", "fsvd_route_ffn_auto",
             "fsvd_session_create", "fsvd_prefill", "fsvd_decode_step", "fsvd_generate", "fsvd_prefill_device",
             "fsvd_decode_step_device", "fsvd_decode_steps_device", "fsvd_generate_device", "fsvd_session_sync", "fsvd_session_stream",
@@ -328,9 +330,17 @@ class Model:
 
     @classmethod
     def load(cls, path, dtype: str = "bf16", device: int = 0) -> "Model":
+        """FSVD15 file -> device (streaming loader; FSVD_LOADER=canonical: host normalize + upload)."""
         h = C.c_void_p()
         _check(lib().fsvd_model_load(str(path).encode(), DTYPE[dtype], device, C.byref(h)))
         return cls(h, dtype)
+
+    @staticmethod
+    def last_load_stats() -> dict:
+        """seconds / payload bytes / pinned staging bytes of this thread's last Model.load."""
+        sec, nb, pb = C.c_double(), C.c_uint64(), C.c_uint64()
+        _check(lib().fsvd_last_load_stats(C.byref(sec), C.byref(nb), C.byref(pb)))
+        return {"seconds": sec.value, "payload_bytes": nb.value, "pinned_bytes": pb.value}
 
     @classmethod
     def from_canonical(cls, canon: Canonical, dtype: str = "bf16", device: int = 0) -> "Model":

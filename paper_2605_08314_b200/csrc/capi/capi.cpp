@@ -1,5 +1,6 @@
 // extern "C" boundary (include/fsvd_c.h): exception -> status mapping,
 // host<->device copies for the host-pointer entry points.
+#include <cstdlib>
 #include <cstring>
 #include <string>
 
@@ -23,6 +24,7 @@ struct fsvd_session {
 namespace {
 
 thread_local std::string g_last_error;
+thread_local fsvd::rt::LoadStats g_last_load;
 
 template <typename F>
 fsvd_status guarded(F&& f) {
@@ -251,10 +253,27 @@ fsvd_status fsvd_model_load(const char* path, fsvd_dtype dtype, int32_t device, 
         need(path, "path");
         need(out, "out");
         check_dtype(dtype);
-        const auto canon = fsvd::normalize<float>(fsvd::read_checkpoint_file(path));
         auto m = std::make_unique<fsvd_model>();
-        m->dm = fsvd::rt::upload_canonical(canon, dtype, device);
+        // streaming loader (no host CanonicalModel); FSVD_LOADER=canonical selects the
+        // read_checkpoint_file -> normalize<float> -> upload path (tests compare the two bitwise)
+        const char* ld = std::getenv("FSVD_LOADER");
+        if (ld && std::string(ld) == "canonical") {
+            const auto canon = fsvd::normalize<float>(fsvd::read_checkpoint_file(path));
+            m->dm = fsvd::rt::upload_canonical(canon, dtype, device);
+        } else {
+            fsvd::rt::LoadStats st;
+            m->dm = fsvd::rt::load_streaming(path, dtype, device, &st);
+            g_last_load = st;
+        }
         *out = m.release();
+    });
+}
+
+fsvd_status fsvd_last_load_stats(double* seconds, uint64_t* payload_bytes, uint64_t* pinned_bytes) {
+    return guarded([&] {
+        if (seconds) *seconds = g_last_load.seconds;
+        if (payload_bytes) *payload_bytes = g_last_load.bytes;
+        if (pinned_bytes) *pinned_bytes = g_last_load.pinned_bytes;
     });
 }
 

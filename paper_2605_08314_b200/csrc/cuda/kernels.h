@@ -130,4 +130,23 @@ struct SynthFill {
 };
 void synth_fill(const SynthFill& f, cudaStream_t s);
 
+// Checkpoint streaming loader (runtime.cu load_streaming): rows [r0, r0 + nrows)
+// of a row-major f32 matrix with `cols` columns (already on the device) go to
+//   mode 0: dst[r * ld + c]                     (embedding rows, vectors)
+//   mode 1: byte offset lay.offset(c, r)        (W^T in the tile layout)
+// in dtype dt, after the family fold of normalize<float> (canonical.cpp):
+// fold 1: x *= 1 / scale[r] (family B), fold 2: x *= scale[c] (family D).
+struct PackArgs {
+    const float* src;
+    long long r0, nrows, cols;
+    int mode;
+    long long ld;
+    WLayout lay;
+    const float* scale;
+    int fold;
+    void* dst;
+    WType dt;
+};
+void pack_f32(const PackArgs& a, cudaStream_t s);
+
 }  // namespace fsvd::k

@@ -3,6 +3,8 @@
 // setter and the synthetic-weight generator.
 #include <math_constants.h>
 
+#include <algorithm>
+
 #include "common.cuh"
 #include "kernels.h"
 
@@ -254,6 +256,39 @@ void gather_last(const float* x, int x_ld, int batch, int T, int d, float* xl, i
 }
 
 void set_int(int* p, int v, cudaStream_t s) { set_int_kernel<<<1, 1, 0, s>>>(p, v); }
+
+// Streaming-loader conversion (one element per thread, grid-stride): the
+// f32 -> bf16 RNE of __float2bfloat16_rn equals the host path's bf16_bits for
+// finite values, and the folds are the IEEE ops normalize<float> performs
+// (inv = 1 / s, then x * inv; x * S), so device factors match the host
+// normalize + upload path bit for bit.
+__global__ void pack_f32_kernel(const PackArgs a) {
+    const long long n = a.nrows * a.cols;
+    for (long long e = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; e < n;
+         e += static_cast<long long>(gridDim.x) * blockDim.x) {
+        const long long lr = e / a.cols, c = e - lr * a.cols, r = a.r0 + lr;
+        float v = a.src[e];
+        if (a.fold == 1) v = __fmul_rn(v, __fdiv_rn(1.0f, a.scale[r]));
+        else if (a.fold == 2) v = __fmul_rn(v, a.scale[c]);
+        char* base = static_cast<char*>(a.dst);
+        if (a.mode == 0) {
+            const long long o = r * a.ld + c;
+            if (a.dt == kBF16) reinterpret_cast<__nv_bfloat16*>(base)[o] = __float2bfloat16_rn(v);
+            else reinterpret_cast<float*>(base)[o] = v;
+        } else {
+            const size_t o = a.lay.offset(static_cast<int>(c), static_cast<int>(r));
+            if (a.dt == kBF16) *reinterpret_cast<__nv_bfloat16*>(base + o) = __float2bfloat16_rn(v);
+            else *reinterpret_cast<float*>(base + o) = v;
+        }
+    }
+}
+
+void pack_f32(const PackArgs& a, cudaStream_t s) {
+    const long long n = a.nrows * a.cols;
+    if (n <= 0) return;
+    const int blocks = static_cast<int>(std::min<long long>((n + 255) / 256, 148LL * 16));
+    pack_f32_kernel<<<blocks, 256, 0, s>>>(a);
+}
 
 void argmax_rows(const float* logits, int V, int batch, int* tokens, int* out, int out_ld, const int* step,
                  cudaStream_t s) {

@@ -14,13 +14,23 @@
 // one launch per phase, per_layer = one CUDA graph per layer, full_step = one
 // graph per step -- the same phases, so bitwise identical outputs.
 // Prefill runs the chunked GEMM path.
+#include <fcntl.h>
+#include <sys/stat.h>
+#include <unistd.h>
+
 #include <algorithm>
+#include <atomic>
+#include <chrono>
 #include <cmath>
+#include <exception>
+#include <mutex>
+#include <set>
 #include <cstdlib>
 #include <cstring>
 #include <thread>
 
 #include "runtime.h"
+#include "fsvd/crc32.hpp"
 
 namespace fsvd::rt {
 
@@ -250,6 +260,326 @@ std::unique_ptr<DeviceModel> upload_canonical(const CanonicalModel<float>& m, fs
     }
     FSVD_CUDA(cudaDeviceSynchronize());
     dm->family = 'A';
+    return dm;
+}
+
+// ------------------------------------------------------ streaming loader --
+namespace {
+
+struct FileEntry {
+    std::string name;
+    std::vector<size_t> shape;
+    size_t off = 0;     // absolute file offset of the data
+    size_t nbytes = 0;
+    uint32_t crc = 0;
+    size_t rows() const { return shape.size() == 2 ? shape[0] : 1; }
+    size_t cols() const { return shape.size() == 2 ? shape[1] : (shape.empty() ? 0 : shape[0]); }
+};
+
+struct PosixFile {
+    int fd = -1;
+    explicit PosixFile(const std::string& path) : fd(::open(path.c_str(), O_RDONLY)) {}
+    ~PosixFile() {
+        if (fd >= 0) ::close(fd);
+    }
+    void read_at(void* dst, size_t n, size_t off) const {
+        char* p = static_cast<char*>(dst);
+        while (n) {
+            const ssize_t r = ::pread(fd, p, n, static_cast<off_t>(off));
+            if (r <= 0) throw FormatError("short read from checkpoint");
+            p += r;
+            n -= static_cast<size_t>(r);
+            off += static_cast<size_t>(r);
+        }
+    }
+};
+
+// One destination of a tensor on the device (see k::PackArgs).
+struct PackJob {
+    const FileEntry* e;
+    int mode;
+    long long ld;
+    k::WLayout lay;
+    const float* scale;  // device vector (fold 1 / 2)
+    int fold;
+    void* dst;
+    k::WType dt;
+};
+
+}  // namespace
+
+std::unique_ptr<DeviceModel> load_streaming(const std::string& path, fsvd_dtype dt, int device, LoadStats* st) {
+    const auto t0 = std::chrono::steady_clock::now();
+    PosixFile f(path);
+    if (f.fd < 0) throw FormatError("cannot open '" + path + "'");
+    struct stat sb {};
+    if (::fstat(f.fd, &sb) != 0) throw FormatError("cannot stat '" + path + "'");
+    const size_t len = static_cast<size_t>(sb.st_size);
+    // ---- container header: the checks and messages of read_checkpoint (checkpoint.cpp) ----
+    constexpr size_t kPrefix = 12;
+    if (len < kPrefix) throw FormatError("file too short for FSVD15 header");
+    uint8_t pre[kPrefix];
+    f.read_at(pre, kPrefix, 0);
+    if (std::memcmp(pre, kCheckpointMagic, 6) != 0) throw FormatError("bad magic (not an FSVD15 file)");
+    uint16_t ver;
+    uint32_t hlen;
+    std::memcpy(&ver, pre + 6, 2);
+    std::memcpy(&hlen, pre + 8, 4);
+    if (ver != kCheckpointVersion) throw FormatError("unsupported version " + std::to_string(ver));
+    if (kPrefix + static_cast<size_t>(hlen) > len) throw FormatError("truncated header");
+    std::string text(hlen, '\0');
+    f.read_at(text.data(), hlen, kPrefix);
+    Checkpoint meta;  // header + names / shapes only (no tensor data)
+    try {
+        meta.header = nlohmann::ordered_json::parse(text);
+    } catch (const nlohmann::json::exception& e) {
+        throw FormatError(std::string("header is not valid JSON: ") + e.what());
+    }
+    auto idx = meta.header.find("tensors");
+    if (idx == meta.header.end() || !idx->is_array()) throw FormatError("header missing tensor index");
+    const size_t base = (kPrefix + hlen + 63) / 64 * 64;
+    std::vector<FileEntry> ents;
+    ents.reserve(idx->size());
+    size_t prev_end = 0;
+    for (const auto& e : *idx) {
+        FileEntry t;
+        size_t off;
+        try {
+            t.name = e.at("name").get<std::string>();
+            if (e.at("dtype").get<std::string>() != "f32") throw FormatError("tensor '" + t.name + "' has unsupported dtype");
+            t.shape = e.at("shape").get<std::vector<size_t>>();
+            off = e.at("offset").get<size_t>();
+            t.crc = e.at("crc32").get<uint32_t>();
+        } catch (const nlohmann::json::exception& ex) {
+            throw FormatError(std::string("malformed tensor index entry: ") + ex.what());
+        }
+        if (off % 64) throw FormatError("tensor '" + t.name + "' offset not 64-byte aligned");
+        if (!ents.empty() && off < prev_end) throw FormatError("tensor '" + t.name + "' overlaps previous tensor");
+        size_t n = t.shape.empty() ? 0 : 1;
+        for (size_t d : t.shape) n *= d;
+        if (n == 0) throw FormatError("tensor '" + t.name + "' has empty shape");
+        t.nbytes = n * sizeof(float);
+        if (base + off + t.nbytes > len) throw FormatError("tensor '" + t.name + "' extends past end of file");
+        t.off = base + off;
+        prev_end = off + t.nbytes;
+        ents.push_back(std::move(t));
+        CheckpointTensor ct;
+        ct.name = ents.back().name;
+        ct.shape = ents.back().shape;
+        meta.tensors.push_back(std::move(ct));
+    }
+    std::map<std::string, const FileEntry*> by_name;
+    for (const auto& e : ents) by_name.emplace(e.name, &e);
+
+    // ---- normalize<float> plan: the checks and messages of canonical.cpp ----
+    const char family = meta.family();
+    ModelConfig c = meta.config();
+    c.validate();
+    auto need_mat = [&](const std::string& n, size_t r, size_t cc) -> const FileEntry* {
+        auto it = by_name.find(n);
+        if (it == by_name.end()) throw NormalizeError("missing tensor '" + n + "'");
+        const FileEntry* e = it->second;
+        if (e->shape.size() != 2 || e->shape[0] != r || e->shape[1] != cc)
+            throw NormalizeError("tensor '" + n + "' has unexpected shape");
+        return e;
+    };
+    auto need_vec = [&](const std::string& n, size_t l) -> const FileEntry* {
+        auto it = by_name.find(n);
+        if (it == by_name.end()) throw NormalizeError("missing tensor '" + n + "'");
+        if (it->second->nbytes / 4 != l) throw NormalizeError("tensor '" + n + "' has unexpected length");
+        return it->second;
+    };
+    auto rank_of = [&](const std::string& n, size_t d_in) -> size_t {
+        auto it = by_name.find(n);
+        if (it == by_name.end()) throw NormalizeError("missing tensor '" + n + "'");
+        if (it->second->shape.size() != 2 || it->second->shape[0] != d_in)
+            throw NormalizeError("tensor '" + n + "' has unexpected shape");
+        return it->second->shape[1];
+    };
+    const FileEntry* emb = need_mat("embedding", c.vocab, c.d_model);
+    const FileEntry* head = need_mat("head", c.d_model, c.vocab);
+    const FileEntry* fgam = need_vec("final_gamma", c.d_model);
+    std::vector<std::array<const FileEntry*, 2>> gam(c.n_layers);
+    for (size_t l = 0; l < c.n_layers; ++l) {
+        const std::string b = "layers." + std::to_string(l) + ".";
+        gam[l] = {need_vec(b + "attn_gamma", c.d_model), need_vec(b + "mlp_gamma", c.d_model)};
+    }
+    struct Proj {
+        const FileEntry *a = nullptr, *b = nullptr, *scale = nullptr;
+        size_t rank = 0;
+        int fold = 0;
+    };
+    std::vector<std::array<Proj, kNumProj>> pj(c.n_layers);
+    std::vector<std::array<size_t, kNumProj>> ranks(c.n_layers);
+    std::vector<std::array<const void*, kNumProj>> keys(c.n_layers);
+    if (family == 'C') {
+        auto it = meta.header.find("layer_groups");
+        if (it == meta.header.end() || !it->is_array() || it->size() != c.n_layers)
+            throw NormalizeError("family C header missing per-layer group references");
+        const auto groups = it->get<std::vector<size_t>>();
+        for (size_t p = 0; p < kNumProj; ++p) {
+            const auto dims = proj_dims(c, p);
+            for (size_t l = 0; l < c.n_layers; ++l) {
+                const std::string g = std::to_string(groups[l]);
+                const std::string name = std::string("shared.") + kProjNames[p] + "." + g + ".A";
+                auto sh = by_name.find(name);
+                if (sh == by_name.end())
+                    throw NormalizeError("layer " + std::to_string(l) + " references unknown group '" + g + "' (no '" +
+                                         name + "')");
+                if (sh->second->shape.size() != 2) throw NormalizeError("tensor '" + name + "' has unexpected shape");
+                Proj& q = pj[l][p];
+                q.a = need_mat(name, dims[0], sh->second->shape[1]);
+                q.rank = q.a->shape[1];
+                q.b = need_mat("layers." + std::to_string(l) + "." + kProjNames[p] + ".B", q.rank, dims[1]);
+                keys[l][p] = q.a;  // one device copy per storage instance
+            }
+        }
+    } else {
+        for (size_t l = 0; l < c.n_layers; ++l)
+            for (size_t p = 0; p < kNumProj; ++p) {
+                const auto dims = proj_dims(c, p);
+                const std::string b = "layers." + std::to_string(l) + "." + kProjNames[p];
+                Proj& q = pj[l][p];
+                const char* an = family == 'A' ? ".A" : family == 'B' ? ".Uf" : ".U";
+                q.rank = rank_of(b + an, dims[0]);
+                q.a = need_mat(b + an, dims[0], q.rank);
+                q.b = need_mat(b + (family == 'A' ? ".B" : ".Vt"), q.rank, dims[1]);
+                if (family == 'B') q.scale = need_vec(b + ".scale", dims[0]), q.fold = 1;
+                if (family == 'D') q.scale = need_vec(b + ".S", q.rank), q.fold = 2;
+                keys[l][p] = nullptr;
+            }
+    }
+    for (size_t l = 0; l < c.n_layers; ++l)
+        for (size_t p = 0; p < kNumProj; ++p) ranks[l][p] = pj[l][p].rank;
+
+    auto dm = std::make_unique<DeviceModel>();
+    init_model_shapes(*dm, c, meta.capacity(), dt, device);
+    allocate(*dm, ranks, keys);
+    dm->family = family;
+
+    // fold vectors (small): read and CRC-check now, zero entries are a NormalizeError (canonical.cpp)
+    std::map<const FileEntry*, float*> dscale;
+    std::vector<void*> scratch;
+    for (size_t l = 0; l < c.n_layers; ++l)
+        for (size_t p = 0; p < kNumProj; ++p) {
+            const FileEntry* se = pj[l][p].scale;
+            if (!se || dscale.count(se)) continue;
+            std::vector<float> v(se->nbytes / 4);
+            f.read_at(v.data(), se->nbytes, se->off);
+            if (crc32(v.data(), se->nbytes) != se->crc) throw FormatError("tensor '" + se->name + "' failed checksum");
+            if (pj[l][p].fold == 1)
+                for (float x : v)
+                    if (!(std::abs(static_cast<double>(x)) > 0.0))
+                        throw NormalizeError("tensor '" + se->name + "' has zero entry");
+            float* d = nullptr;
+            FSVD_CUDA(cudaMalloc(&d, se->nbytes));
+            scratch.push_back(d);
+            FSVD_CUDA(cudaMemcpy(d, v.data(), se->nbytes, cudaMemcpyHostToDevice));
+            dscale[se] = d;
+        }
+
+    // ---- jobs: every tensor once, to its device destination ----
+    const k::WType wt = dm->wt;
+    std::vector<PackJob> jobs;
+    jobs.push_back({emb, 0, dm->ldd, {}, nullptr, 0, const_cast<void*>(dm->emb), wt});
+    jobs.push_back({head, 1, 0, dm->head_t.layout(dm->esize), nullptr, 0, const_cast<void*>(dm->head_t.w), wt});
+    jobs.push_back({fgam, 0, static_cast<long long>(c.d_model), {}, nullptr, 0, const_cast<float*>(dm->final_gamma), k::kF32});
+    std::set<const void*> done;
+    for (size_t l = 0; l < c.n_layers; ++l) {
+        const DeviceLayer& D = dm->layers[l];
+        for (size_t p = 0; p < kNumProj; ++p) {
+            const Proj& q = pj[l][p];
+            if (done.insert(D.at[p].w).second)
+                jobs.push_back({q.a, 1, 0, D.at[p].layout(dm->esize), q.scale ? dscale[q.scale] : nullptr, q.fold,
+                                const_cast<void*>(D.at[p].w), wt});
+            jobs.push_back({q.b, 1, 0, D.bt[p].layout(dm->esize), nullptr, 0, const_cast<void*>(D.bt[p].w), wt});
+        }
+        jobs.push_back({gam[l][0], 0, static_cast<long long>(c.d_model), {}, nullptr, 0, const_cast<float*>(D.attn_gamma), k::kF32});
+        jobs.push_back({gam[l][1], 0, static_cast<long long>(c.d_model), {}, nullptr, 0, const_cast<float*>(D.mlp_gamma), k::kF32});
+    }
+    std::sort(jobs.begin(), jobs.end(), [](const PackJob& a, const PackJob& b) { return a.e->nbytes > b.e->nbytes; });
+
+    // ---- workers: pread -> pinned chunk (+ CRC) -> H2D -> pack kernel, double buffered ----
+    constexpr size_t kChunk = 32ull << 20;
+    const int nw = static_cast<int>(std::max<size_t>(1, std::min<size_t>({8, jobs.size(), std::max(1u, std::thread::hardware_concurrency() / 2)})));
+    std::atomic<size_t> next{0};
+    std::atomic<uint64_t> total{0};
+    std::mutex err_mu;
+    std::exception_ptr err;
+    auto worker = [&]() {
+        cudaStream_t s = nullptr;
+        void* host[2] = {nullptr, nullptr};
+        float* dev[2] = {nullptr, nullptr};
+        cudaEvent_t ev[2] = {nullptr, nullptr};
+        try {
+            FSVD_CUDA(cudaSetDevice(device));
+            FSVD_CUDA(cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking));
+            for (int b = 0; b < 2; ++b) {
+                FSVD_CUDA(cudaMallocHost(&host[b], kChunk));
+                FSVD_CUDA(cudaMalloc(&dev[b], kChunk));
+                FSVD_CUDA(cudaEventCreateWithFlags(&ev[b], cudaEventDisableTiming));
+            }
+            bool used[2] = {false, false};
+            int b = 0;
+            for (size_t j; (j = next.fetch_add(1)) < jobs.size();) {
+                const PackJob& job = jobs[j];
+                const FileEntry& e = *job.e;
+                const size_t rows = e.rows(), cols = e.cols(), row_bytes = cols * 4;
+                const size_t rows_per = std::max<size_t>(1, kChunk / row_bytes);
+                if (row_bytes > kChunk) throw ConfigError("checkpoint row larger than the loader's staging chunk");
+                uint32_t crc = 0;
+                for (size_t r0 = 0; r0 < rows; r0 += rows_per) {
+                    const size_t nr = std::min(rows_per, rows - r0), nb = nr * row_bytes;
+                    if (used[b]) FSVD_CUDA(cudaEventSynchronize(ev[b]));
+                    f.read_at(host[b], nb, e.off + r0 * row_bytes);
+                    crc = crc32_update(crc, host[b], nb);
+                    FSVD_CUDA(cudaMemcpyAsync(dev[b], host[b], nb, cudaMemcpyHostToDevice, s));
+                    k::PackArgs a{};
+                    a.src = dev[b];
+                    a.r0 = static_cast<long long>(r0);
+                    a.nrows = static_cast<long long>(nr);
+                    a.cols = static_cast<long long>(cols);
+                    a.mode = job.mode;
+                    a.ld = job.ld;
+                    a.lay = job.lay;
+                    a.scale = job.scale;
+                    a.fold = job.fold;
+                    a.dst = job.dst;
+                    a.dt = job.dt;
+                    k::pack_f32(a, s);
+                    FSVD_CUDA(cudaGetLastError());
+                    FSVD_CUDA(cudaEventRecord(ev[b], s));
+                    used[b] = true;
+                    b ^= 1;
+                    total += nb;
+                }
+                if (crc != e.crc) throw FormatError("tensor '" + e.name + "' failed checksum");
+            }
+            FSVD_CUDA(cudaStreamSynchronize(s));
+        } catch (...) {
+            std::lock_guard<std::mutex> g(err_mu);
+            if (!err) err = std::current_exception();
+            next = jobs.size();
+        }
+        if (s) cudaStreamSynchronize(s);
+        for (int b = 0; b < 2; ++b) {
+            if (host[b]) cudaFreeHost(host[b]);
+            if (dev[b]) cudaFree(dev[b]);
+            if (ev[b]) cudaEventDestroy(ev[b]);
+        }
+        if (s) cudaStreamDestroy(s);
+    };
+    std::vector<std::thread> ts;
+    for (int w = 0; w < nw; ++w) ts.emplace_back(worker);
+    for (auto& t : ts) t.join();
+    for (void* p : scratch) cudaFree(p);
+    if (err) std::rethrow_exception(err);
+    FSVD_CUDA(cudaDeviceSynchronize());
+    if (st) {
+        st->seconds = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+        st->bytes = total.load();
+        st->pinned_bytes = static_cast<uint64_t>(nw) * 2 * kChunk;
+    }
     return dm;
 }
 

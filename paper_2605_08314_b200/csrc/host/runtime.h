@@ -78,6 +78,17 @@ struct DeviceModel {
 
 std::unique_ptr<DeviceModel> upload_canonical(const CanonicalModel<float>& m, fsvd_dtype dt, int device);
 std::unique_ptr<DeviceModel> generate_synthetic(const SynthSpec& spec, fsvd_dtype dt, int device);
+// FSVD15 file -> device model without a host CanonicalModel (load_streaming in
+// runtime.cu): positioned reads into pinned staging buffers, CRC-32 checked on
+// the fly, f32 -> weight dtype + family fold on the device straight into the
+// tile layout. Same validation and errors as read_checkpoint_file +
+// normalize<float>; device factors bitwise equal to upload_canonical's.
+struct LoadStats {
+    double seconds = 0;
+    uint64_t bytes = 0;        // payload bytes read
+    uint64_t pinned_bytes = 0; // host staging held at once
+};
+std::unique_ptr<DeviceModel> load_streaming(const std::string& path, fsvd_dtype dt, int device, LoadStats* st = nullptr);
 void copy_factor(const DeviceModel& m, size_t layer, size_t proj, bool b, float* out, size_t count);
 
 struct StepStats {
