@@ -52,12 +52,23 @@ typedef enum fsvd_ffn_backend {
 
 /* SPEC.md:294 Session.plan_mode. PER_LAYER = one CUDA graph per decoder layer
  * (SPEC.md:401-418 full_layer plans); FULL_STEP = one graph per decode step
- * (extension; same kernels, same order). */
+ * (extension; same kernels, same order); SPLIT = two graphs per layer
+ * (attention body, MLP body) with an explicit boundary copy between them
+ * (SPEC.md:404-418 split plans). */
 typedef enum fsvd_plan_mode {
     FSVD_PLAN_EAGER = 0,
     FSVD_PLAN_PER_LAYER = 1,
-    FSVD_PLAN_FULL_STEP = 2
+    FSVD_PLAN_FULL_STEP = 2,
+    FSVD_PLAN_SPLIT = 3
 } fsvd_plan_mode;
+
+/* SPEC.md:294 Session.attn_route. LOWRANK_HISTORY (ablation)
+ * keeps the rank-space K/V history and reconstructs dense K, V (+ RoPE) for
+ * every cached position at every decode step; eager plan only. */
+typedef enum fsvd_attn_route {
+    FSVD_ATTN_DENSE_KV = 0,
+    FSVD_ATTN_LOWRANK_HISTORY = 1
+} fsvd_attn_route;
 
 typedef struct fsvd_config {
     uint64_t n_layers, d_model, n_heads, d_head, d_ff, vocab;
@@ -81,6 +92,7 @@ typedef struct fsvd_session_opts {
     uint64_t capacity;        /* KV positions per sequence; 0 = model capacity */
     fsvd_ffn_backend ffn;
     fsvd_plan_mode plan;
+    fsvd_attn_route attn_route;
 } fsvd_session_opts;
 
 /* SPEC.md:299-302 StepStats, plus device-side counters. */
@@ -92,6 +104,7 @@ typedef struct fsvd_step_stats {
     uint64_t allocs;           /* device allocations after session create */
     uint64_t copy_bytes;       /* host<->device bytes moved by the API calls */
     uint64_t last_dispatches;  /* dispatches of the last decode step */
+    uint64_t recon_flops;      /* K/V reconstruction FLOPs of the lowrank_history route (0 for dense_kv) */
 } fsvd_step_stats;
 
 typedef struct fsvd_canonical fsvd_canonical; /* host CanonicalModel<float> */
@@ -117,6 +130,8 @@ fsvd_status fsvd_canonical_shared_count(const fsvd_canonical* c, uint64_t* n);
 /* 1 if layers (l0, l1) alias the same A storage for projection proj. */
 fsvd_status fsvd_canonical_aliased(const fsvd_canonical* c, uint64_t l0, uint64_t l1, uint32_t proj, int32_t* out);
 fsvd_status fsvd_canonical_destroy(fsvd_canonical* c);
+/* Write a normalized model as a family-A FSVD15 file (the CLI's `normalize`). */
+fsvd_status fsvd_canonical_write_file(const fsvd_canonical* c, const char* path);
 /* Materialize a synthetic checkpoint as an FSVD15 file. */
 fsvd_status fsvd_synthetic_write_file(const fsvd_synth_spec* spec, const char* path);
 

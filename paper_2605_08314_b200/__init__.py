@@ -80,7 +80,8 @@ _ERRORS = {e.status: e for e in (ShapeError, RankError, NumericError, CapacityEr
 # ------------------------------------------------------------------ enums --
 DTYPE = {"f32": 0, "fp32": 0, "float32": 0, "bf16": 1, "bfloat16": 1}
 FFN = {"auto": 0, "no_merge": 1, "packed": 2}
-PLAN = {"eager": 0, "per_layer": 1, "full_step": 2}
+PLAN = {"eager": 0, "per_layer": 1, "full_step": 2, "split": 3}
+ATTN = {"dense_kv": 0, "lowrank_history": 1}
 FFN_NAMES = {v: k for k, v in FFN.items()}
 PLAN_NAMES = {v: k for k, v in PLAN.items()}
 PROJ = ("q", "k", "v", "o", "up", "gate", "down")
@@ -98,13 +99,14 @@ class _Synth(C.Structure):
 
 
 class _Opts(C.Structure):
-    _fields_ = [("batch", C.c_uint32), ("capacity", C.c_uint64), ("ffn", C.c_int), ("plan", C.c_int)]
+    _fields_ = [("batch", C.c_uint32), ("capacity", C.c_uint64), ("ffn", C.c_int), ("plan", C.c_int),
+                ("attn_route", C.c_int)]
 
 
 class _Stats(C.Structure):
     _fields_ = [("steps", C.c_uint64), ("dispatches", C.c_uint64), ("kernel_launches", C.c_uint64),
                 ("graph_launches", C.c_uint64), ("allocs", C.c_uint64), ("copy_bytes", C.c_uint64),
-                ("last_dispatches", C.c_uint64)]
+                ("last_dispatches", C.c_uint64), ("recon_flops", C.c_uint64)]
 
 
 @dataclass(frozen=True)
@@ -180,6 +182,7 @@ def lib() -> C.CDLL:
         "fsvd_canonical_aliased": ([vp, u64, u64, C.c_uint32, i32p], C.c_int),
         "fsvd_canonical_destroy": ([vp], C.c_int),
         "fsvd_synthetic_write_file": ([C.POINTER(_Synth), C.c_char_p], C.c_int),
+        "fsvd_canonical_write_file": ([vp, C.c_char_p], C.c_int),
         "fsvd_model_load": ([C.c_char_p, C.c_int, i32, C.POINTER(vp)], C.c_int),
         "fsvd_last_load_stats": ([C.POINTER(C.c_double), C.POINTER(C.c_uint64), C.POINTER(C.c_uint64)], C.c_int),
         "fsvd_model_from_canonical": ([vp, C.c_int, i32, C.POINTER(vp)], C.c_int),
@@ -219,7 +222,7 @@ def exported_symbols() -> list[str]:
     return ["fsvd_last_error", "fsvd_version", "fsvd_canonical_load_file", "fsvd_canonical_load_bytes",
             "fsvd_canonical_synthetic", "fsvd_canonical_config", "fsvd_canonical_rank", "fsvd_canonical_copy",
             "fsvd_canonical_shared_count", "fsvd_canonical_aliased", "fsvd_canonical_destroy",
-            "fsvd_synthetic_write_file", "fsvd_model_load", "fsvd_last_load_stats", "fsvd_model_from_canonical",
+            "fsvd_canonical_write_file", "fsvd_synthetic_write_file", "fsvd_model_load", "fsvd_last_load_stats", "fsvd_model_from_canonical",
             "fsvd_model_synthetic",
             "fsvd_model_info", "fsvd_model_copy_factor", "fsvd_model_destroy", "fsvd_route_ffn_auto",
             "fsvd_session_create", "fsvd_prefill", "fsvd_decode_step", "fsvd_generate", "fsvd_prefill_device",
@@ -297,6 +300,10 @@ class Canonical:
         out = np.empty(shape, dtype=np.float32)
         _check(lib().fsvd_canonical_copy(self._h, name.encode(), _f32p(out), out.size))
         return out
+
+    def write_file(self, path) -> None:
+        """Normalized model -> family-A FSVD15 file (canonical.cpp export_family_a)."""
+        _check(lib().fsvd_canonical_write_file(self._h, str(path).encode()))
 
     def shared_count(self) -> int:
         n = C.c_uint64()
@@ -387,18 +394,20 @@ class StepStats:
     allocs: int
     copy_bytes: int
     last_dispatches: int
+    recon_flops: int = 0  # lowrank_history route: K/V reconstruction FLOPs
 
 
 class Session:
     """SPEC.md:293-298 Session: KV cache + workspace + plans for `batch`
     independent sequences advanced in lock step on one GPU."""
 
-    def __init__(self, model: Model, batch: int = 1, capacity: int = 0, ffn: str = "auto", plan: str = "eager"):
+    def __init__(self, model: Model, batch: int = 1, capacity: int = 0, ffn: str = "auto", plan: str = "eager",
+                 attn_route: str = "dense_kv"):
         self.model = model
         self.batch = batch
         self._cfg = model.config
         h = C.c_void_p()
-        o = _Opts(batch, capacity, FFN[ffn], PLAN[plan])
+        o = _Opts(batch, capacity, FFN[ffn], PLAN[plan], ATTN[attn_route])
         _check(lib().fsvd_session_create(model._h, C.byref(o), C.byref(h)))
         self._h = h
 
@@ -459,7 +468,7 @@ class Session:
         s = _Stats()
         _check(lib().fsvd_session_stats(self._h, C.byref(s)))
         return StepStats(s.steps, s.dispatches, s.kernel_launches, s.graph_launches, s.allocs, s.copy_bytes,
-                         s.last_dispatches)
+                         s.last_dispatches, s.recon_flops)
 
     def resolved(self) -> tuple[str, str]:
         f, p = C.c_int(), C.c_int()

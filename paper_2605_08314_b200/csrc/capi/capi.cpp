@@ -239,6 +239,14 @@ fsvd_status fsvd_canonical_destroy(fsvd_canonical* c) {
     return guarded([&] { delete c; });
 }
 
+fsvd_status fsvd_canonical_write_file(const fsvd_canonical* c, const char* path) {
+    return guarded([&] {
+        need(c, "canonical");
+        need(path, "path");
+        fsvd::write_checkpoint_file(fsvd::export_family_a(c->m), path);
+    });
+}
+
 fsvd_status fsvd_synthetic_write_file(const fsvd_synth_spec* spec, const char* path) {
     return guarded([&] {
         need(spec, "spec");
@@ -327,7 +335,7 @@ fsvd_status fsvd_model_destroy(fsvd_model* m) {
 fsvd_status fsvd_route_ffn_auto(fsvd_plan_mode plan, fsvd_ffn_backend requested, fsvd_ffn_backend* out) {
     return guarded([&] {
         need(out, "out");
-        if (plan < FSVD_PLAN_EAGER || plan > FSVD_PLAN_FULL_STEP) throw fsvd::ConfigError("unknown plan mode");
+        if (plan < FSVD_PLAN_EAGER || plan > FSVD_PLAN_SPLIT) throw fsvd::ConfigError("unknown plan mode");
         if (requested < FSVD_FFN_AUTO || requested > FSVD_FFN_PACKED) throw fsvd::ConfigError("unknown ffn backend");
         *out = fsvd::rt::route_ffn_auto(plan, requested);
     });
@@ -467,7 +475,8 @@ fsvd_status fsvd_session_stats(const fsvd_session* s, fsvd_step_stats* st) {
         need(s, "session");
         need(st, "stats");
         const auto& x = s->s->stats();
-        *st = {x.steps, x.dispatches, x.kernel_launches, x.graph_launches, x.allocs, x.copy_bytes, x.last_dispatches};
+        *st = {x.steps, x.dispatches, x.kernel_launches, x.graph_launches, x.allocs, x.copy_bytes, x.last_dispatches,
+               x.recon_flops};
     });
 }
 

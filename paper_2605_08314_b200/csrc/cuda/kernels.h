@@ -149,4 +149,10 @@ struct PackArgs {
 };
 void pack_f32(const PackArgs& a, cudaStream_t s);
 
+// lowrank_history route: rank-space rows (b, t) of a [B*T][src_ld] buffer,
+// columns [col0, col0 + ncols), to dst[b * dst_bstride + (p0 + t) * dst_ld + j]
+// (p0 = *p0_dev if given); esize-byte elements.
+void copy_rows_at(const void* src, int src_ld, int col0, int ncols, void* dst, long long dst_bstride, int dst_ld,
+                  int batch, int T, int p0, const int* p0_dev, int esize, cudaStream_t s);
+
 }  // namespace fsvd::k

@@ -283,6 +283,26 @@ __global__ void pack_f32_kernel(const PackArgs a) {
     }
 }
 
+template <typename E>
+__global__ void copy_rows_at_kernel(const E* src, int src_ld, int col0, int ncols, E* dst, long long dst_bstride,
+                                    int dst_ld, int T, int p0, const int* p0_dev) {
+    const int row = blockIdx.x, b = row / T, t = row - b * T;
+    const int p = (p0_dev ? *p0_dev : p0) + t;
+    for (int j = threadIdx.x; j < ncols; j += blockDim.x)
+        dst[b * dst_bstride + static_cast<long long>(p) * dst_ld + j] = src[static_cast<long long>(row) * src_ld + col0 + j];
+}
+
+void copy_rows_at(const void* src, int src_ld, int col0, int ncols, void* dst, long long dst_bstride, int dst_ld,
+                  int batch, int T, int p0, const int* p0_dev, int esize, cudaStream_t s) {
+    if (esize == 2)
+        copy_rows_at_kernel<uint16_t><<<batch * T, 256, 0, s>>>(static_cast<const uint16_t*>(src), src_ld, col0, ncols,
+                                                               static_cast<uint16_t*>(dst), dst_bstride, dst_ld, T, p0,
+                                                               p0_dev);
+    else
+        copy_rows_at_kernel<float><<<batch * T, 256, 0, s>>>(static_cast<const float*>(src), src_ld, col0, ncols,
+                                                            static_cast<float*>(dst), dst_bstride, dst_ld, T, p0, p0_dev);
+}
+
 void pack_f32(const PackArgs& a, cudaStream_t s) {
     const long long n = a.nrows * a.cols;
     if (n <= 0) return;

@@ -702,7 +702,7 @@ fsvd_ffn_backend route_ffn_auto(fsvd_plan_mode plan, fsvd_ffn_backend requested)
     // per_layer -> packed, split -> no_merge. The full-step graph is a
     // layer-tail graph superset, so it routes like per_layer.
     if (requested != FSVD_FFN_AUTO) return requested;
-    return plan == FSVD_PLAN_EAGER ? FSVD_FFN_NO_MERGE : FSVD_FFN_PACKED;
+    return plan == FSVD_PLAN_EAGER || plan == FSVD_PLAN_SPLIT ? FSVD_FFN_NO_MERGE : FSVD_FFN_PACKED;
 }
 
 void* Session::dalloc(size_t bytes) {
@@ -744,12 +744,22 @@ void Session::init(const fsvd_session_opts& o) {
     // layer engine (FSVD_BATCHED=1 forces it for any batch)
     batched_ = B_ > 2;
     if (const char* e = std::getenv("FSVD_BATCHED"); e && e[0] == '1') batched_ = true;
+    if (o.attn_route != FSVD_ATTN_DENSE_KV && o.attn_route != FSVD_ATTN_LOWRANK_HISTORY)
+        throw ConfigError("unknown attention route");
+    attn_route_ = o.attn_route;
+    if (attn_route_ == FSVD_ATTN_LOWRANK_HISTORY) {
+        // per-step reconstruction GEMMs over the whole history: shapes change every
+        // step, so no static plan can hold them (SPEC.md:405 capture error)
+        if (o.plan != FSVD_PLAN_EAGER)
+            throw ConfigError("lowrank_history attention route needs the eager plan (dynamic shapes)");
+        batched_ = true;  // the layer engine (GEMM launches) hosts the reconstruction
+    }
     if (!batched_ && m_->cfg.d_model > 8192)
         throw ConfigError("d_model > 8192 is not supported by the decode megakernel");
     if (!(c.d_head == 32 || c.d_head == 64 || c.d_head == 128))
         throw ConfigError("d_head must be 32, 64 or 128 for the sm_100a kernels");
     cap_ = o.capacity ? o.capacity : (m->capacity ? m->capacity : 8192);
-    if (o.plan < FSVD_PLAN_EAGER || o.plan > FSVD_PLAN_FULL_STEP) throw ConfigError("unknown plan mode");
+    if (o.plan < FSVD_PLAN_EAGER || o.plan > FSVD_PLAN_SPLIT) throw ConfigError("unknown plan mode");
     if (o.ffn < FSVD_FFN_AUTO || o.ffn > FSVD_FFN_PACKED) throw ConfigError("unknown ffn backend");
     plan_ = o.plan;
     ffn_ = route_ffn_auto(plan_, o.ffn);
@@ -800,6 +810,14 @@ void Session::init(const fsvd_session_opts& o) {
     mk_grid_ = std::min(mk_grid_, 256);
     if (const char* e = std::getenv("FSVD_MK_EXACT")) mk_exact_ = e[0] == '1';  // attention merge scratch is sized for <= 256 pieces per head
     mk_splits_ = mk_grid_;  // attention partial slots per head: one per contributing CTA
+    if (attn_route_ == FSVD_ATTN_LOWRANK_HISTORY) {
+        for (const auto& Ly : m->layers) ld_hist_ = std::max({ld_hist_, Ly.r[kK], Ly.r[kV]});
+        ld_hist_ = pad8(ld_hist_);
+        const size_t hb = static_cast<size_t>(L) * B_ * cap_ * ld_hist_ * m->esize;
+        hist_k_ = dalloc(hb);
+        hist_v_ = dalloc(hb);
+    }
+    if (plan_ == FSVD_PLAN_SPLIT) split_buf_ = dalloc(4ull * B_ * m->ldd);
     if (batched_) {
         ensure_prefill_workspace(B_);
         dec_splits_ = k::attn_decode_splits(B_, static_cast<int>(H), static_cast<int>(cap_));
@@ -978,6 +996,7 @@ void Session::add_layer_phases(size_t l, const float* next_gamma) {
         g.gamma = L.mlp_gamma;
     }
     // FFN input side: packed = one projection over [A_up | A_gate]
+    ph_ffn_begin_.push_back(static_cast<int>(h_phases_.size()));
     if (ffn_ == FSVD_FFN_PACKED) {
         k::MkGemv& g = add_gemv({seg(L.at[kUp], 0, 0, 0), seg(L.at[kGate], 0, 0, 0)}, 0, xpl_, xres_, k::kOutPlanes);
         g.out = pug_;
@@ -1010,6 +1029,7 @@ void Session::build_program() {
     rec_chunks_ = 0;
     ph_layer_begin_.clear();
     ph_layer_end_.clear();
+    ph_ffn_begin_.clear();
     // activation planes (each a phase's input, written by its producer's finalizers)
     int lq = 0, lo = 0, lug = 0, ld = 0;
     for (const auto& Ly : m.layers) {
@@ -1184,10 +1204,19 @@ void Session::mk_decode(int32_t* d_out, int out_ld) {
         stats_.dispatches += 1;
         return;
     }
-    // per-layer plans: layer 0 .. L-1 (layer 0 gathers the embedding), [head + argmax]
+    // per-layer plans: layer 0 .. L-1 (layer 0 gathers the embedding), [head + argmax];
+    // split plans: [attention body], [MLP body] per layer
+    const bool split = plan_ == FSVD_PLAN_SPLIT;
     if (layer_graphs_.empty()) {
         std::vector<std::pair<int, int>> ranges;
-        for (int l = 0; l < L; ++l) ranges.push_back({ph_layer_begin_[l], ph_layer_end_[l]});
+        for (int l = 0; l < L; ++l) {
+            if (split) {
+                ranges.push_back({ph_layer_begin_[l], ph_ffn_begin_[l]});
+                ranges.push_back({ph_ffn_begin_[l], ph_layer_end_[l]});
+            } else {
+                ranges.push_back({ph_layer_begin_[l], ph_layer_end_[l]});
+            }
+        }
         ranges.push_back({ph_head_, ph_argmax_ + 1});
         for (auto [b, e] : ranges) {
             cudaGraph_t g;
@@ -1200,9 +1229,24 @@ void Session::mk_decode(int32_t* d_out, int out_ld) {
             layer_graphs_.push_back(ge);
         }
     }
-    for (auto g : layer_graphs_) FSVD_CUDA(cudaGraphLaunch(g, stream_));
+    if (!split) {
+        for (auto g : layer_graphs_) FSVD_CUDA(cudaGraphLaunch(g, stream_));
+        stats_.graph_launches += layer_graphs_.size();
+        stats_.dispatches += layer_graphs_.size();
+        return;
+    }
+    // split: the host boundary between a layer's attention and MLP graphs is an explicit
+    // copy of the residual stream (the "graph-boundary traffic" of SPEC.md:406, Fig. 6)
+    const size_t cb = 4ull * B_ * m_->ldd;
+    for (int l = 0; l < L; ++l) {
+        FSVD_CUDA(cudaGraphLaunch(layer_graphs_[2 * l], stream_));
+        FSVD_CUDA(cudaMemcpyAsync(split_buf_, xres_, cb, cudaMemcpyDeviceToDevice, stream_));
+        FSVD_CUDA(cudaGraphLaunch(layer_graphs_[2 * l + 1], stream_));
+        stats_.copy_bytes += cb;
+    }
+    FSVD_CUDA(cudaGraphLaunch(layer_graphs_.back(), stream_));
     stats_.graph_launches += layer_graphs_.size();
-    stats_.dispatches += layer_graphs_.size();
+    stats_.dispatches += layer_graphs_.size() + L;
 }
 
 void Session::decode_step(const int32_t* d_tokens, float* d_logits) {
@@ -1329,10 +1373,54 @@ void Session::layers_forward(int M, int Tc, int p0, const int* p0_dev) {
              {seg(L.at[kQ], 0, 0, k::kEpiStore), seg(L.at[kK], 0, rq, k::kEpiStore),
               seg(L.at[kV], 0, rq + rk, k::kEpiStore)},
              k::kGemmStore, pf_pqkv_, ld_qkv_);
-        gemm(pf_pqkv_, ld_qkv_, 3,
-             {seg(L.bt[kQ], 0, 0, k::kEpiRopeQ), seg(L.bt[kK], rq, 0, k::kEpiRopeK),
-              seg(L.bt[kV], rq + rk, 0, k::kEpiV)},
-             k::kGemmQKV, pf_q_, ldd, kc, vc);
+        if (attn_route_ == FSVD_ATTN_LOWRANK_HISTORY) {
+            // record the pre-RoPE rank-space k / v rows of these positions
+            const long long hstride = static_cast<long long>(cap_) * ld_hist_;
+            char* hk = static_cast<char*>(hist_k_) + l * B_ * hstride * es;
+            char* hv = static_cast<char*>(hist_v_) + l * B_ * hstride * es;
+            k::copy_rows_at(pf_pqkv_, ld_qkv_, rq, L.r[kK], hk, hstride, ld_hist_, B_, Tc, p0, p0_dev,
+                            static_cast<int>(es), stream_);
+            k::copy_rows_at(pf_pqkv_, ld_qkv_, rq + rk, L.r[kV], hv, hstride, ld_hist_, B_, Tc, p0, p0_dev,
+                            static_cast<int>(es), stream_);
+        }
+        if (attn_route_ == FSVD_ATTN_LOWRANK_HISTORY && Tc == 1) {
+            // decode: q from its rank-space row; the whole dense K / V history is rebuilt from
+            // the rank-space history -- K = P_k B_k with RoPE at every position, V = P_v B_v --
+            // then attended like dense_kv (numerically the same, deliberately cost-inferior)
+            gemm(pf_pqkv_, ld_qkv_, 1, {seg(L.bt[kQ], 0, 0, k::kEpiRopeQ)}, k::kGemmQKV, pf_q_, ldd, kc, vc);
+            const int len = static_cast<int>(position_) + 1;
+            const long long hstride = static_cast<long long>(cap_) * ld_hist_;
+            for (int b = 0; b < B_; ++b) {
+                for (int kv = 0; kv < 2; ++kv) {
+                    k::GemmArgs g{};
+                    g.x = static_cast<char*>(kv ? hist_v_ : hist_k_) + (l * B_ + b) * hstride * es;
+                    g.x_ld = ld_hist_;
+                    g.M = len;
+                    g.seg[0] = seg(kv ? L.bt[kV] : L.bt[kK], 0, 0, kv ? k::kEpiV : k::kEpiRopeK);
+                    g.nseg = 1;
+                    g.epi = k::kGemmQKV;
+                    g.y = pf_q_;
+                    g.y_ld = ldd;
+                    g.rope = rope_;
+                    g.p0 = 0;
+                    g.T = len;
+                    g.d_head = static_cast<int>(c.d_head);
+                    g.n_heads = static_cast<int>(c.n_heads);
+                    g.kcache = kc + b * cache_bstride_ * es;
+                    g.vcache = vc + b * cache_bstride_ * es;
+                    g.cache_bstride = cache_bstride_;
+                    g.cache_hstride = cache_hstride_;
+                    k::gemm(m.wt, g, stream_);
+                    stats_.recon_flops += 2ull * len * (kv ? L.r[kV] : L.r[kK]) * d;
+                }
+            }
+            launches_this_step_ += 2 * B_;
+        } else {
+            gemm(pf_pqkv_, ld_qkv_, 3,
+                 {seg(L.bt[kQ], 0, 0, k::kEpiRopeQ), seg(L.bt[kK], rq, 0, k::kEpiRopeK),
+                  seg(L.bt[kV], rq + rk, 0, k::kEpiV)},
+                 k::kGemmQKV, pf_q_, ldd, kc, vc);
+        }
         {
             k::AttnPrefillArgs a{};
             a.q = pf_q_;
@@ -1356,6 +1444,11 @@ void Session::layers_forward(int M, int Tc, int p0, const int* p0_dev) {
         }
         gemm(pf_att_, ldd, 1, {seg(L.at[kO], 0, 0, k::kEpiStore)}, k::kGemmStore, pf_po_, ld_o_);
         gemm(pf_po_, ld_o_, 1, {seg(L.bt[kO], 0, 0, k::kEpiStore)}, k::kGemmAddF32, pf_x_, ldd);
+        if (plan_ == FSVD_PLAN_SPLIT && Tc == 1) {  // split plan: attention | MLP boundary copy
+            FSVD_CUDA(cudaMemcpyAsync(split_buf_, pf_x_, 4ull * M * ldd, cudaMemcpyDeviceToDevice, stream_));
+            stats_.copy_bytes += 4ull * M * ldd;
+            stats_.dispatches += 1;
+        }
         k::rmsnorm_rows(m.wt, pf_x_, ldd, L.mlp_gamma, eps, M, d, pf_xn_, ldd, stream_);
         if (ffn_ == FSVD_FFN_PACKED) {
             gemm(pf_xn_, ldd, 2, {seg(L.at[kUp], 0, 0, k::kEpiStore), seg(L.at[kGate], 0, L.rp[kUp], k::kEpiStore)},
@@ -1411,7 +1504,7 @@ void Session::batched_decode(int32_t* d_out, int out_ld) {
         head_rows(pf_x_, d_out, out_ld, 1);
     };
     launches_this_step_ = 0;
-    if (plan_ == FSVD_PLAN_EAGER) {
+    if (plan_ == FSVD_PLAN_EAGER || plan_ == FSVD_PLAN_SPLIT) {  // (split: eager launches + boundary copies)
         body();
         const uint64_t n = launches_this_step_ + 1 + 10ull * m.cfg.n_layers;
         stats_.dispatches += n;

@@ -93,7 +93,7 @@ void copy_factor(const DeviceModel& m, size_t layer, size_t proj, bool b, float*
 
 struct StepStats {
     uint64_t steps = 0, dispatches = 0, kernel_launches = 0, graph_launches = 0, allocs = 0, copy_bytes = 0,
-             last_dispatches = 0;
+             last_dispatches = 0, recon_flops = 0;
 };
 
 fsvd_ffn_backend route_ffn_auto(fsvd_plan_mode plan, fsvd_ffn_backend requested);
@@ -120,6 +120,7 @@ class Session {
     StepStats& stats() { return stats_; }
     fsvd_ffn_backend ffn() const { return ffn_; }
     fsvd_plan_mode plan() const { return plan_; }
+    fsvd_attn_route attn_route() const { return attn_route_; }
     // device staging for host-pointer API calls (grown on demand)
     void* staging(size_t bytes);
     // copies the last traced full step: [grid][phases][4] ns stamps; returns phases
@@ -158,6 +159,15 @@ class Session {
     size_t cap_;
     fsvd_ffn_backend ffn_;
     fsvd_plan_mode plan_;
+    fsvd_attn_route attn_route_ = FSVD_ATTN_DENSE_KV;
+    // lowrank_history route: pre-RoPE rank-space K / V history
+    // [L][B][cap][ld_hist_], rebuilt into the dense cache every decode step
+    void* hist_k_ = nullptr;
+    void* hist_v_ = nullptr;
+    int ld_hist_ = 0;
+    // split plan: first FFN phase of each layer, boundary-copy buffer
+    std::vector<int> ph_ffn_begin_;
+    void* split_buf_ = nullptr;
     cudaStream_t stream_ = nullptr;
     std::vector<void*> allocations_;
     StepStats stats_;
