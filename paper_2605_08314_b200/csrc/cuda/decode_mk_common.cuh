@@ -106,8 +106,8 @@ namespace fsvd::k {
 // of one (output tile, sub) -- sub 1 = the gate half of a dual tile. CTA c
 // of G owns units [total*c/G, total*(c+1)/G); its chunks are <= kChunkLines
 // units of one run, starting at the run start or at the CTA's first unit.
-// Split products are 64-bit; the per-chunk walk is incremental (ChunkIter)
-// -- no divisions on the streaming path.
+// All arithmetic is 32-bit (total * G < 2^32); the per-chunk walk is
+// incremental (ChunkIter) -- no divisions on the streaming path.
 struct MkSplit {
     int total;
     int nseg, dual;
@@ -150,7 +150,7 @@ struct MkSplit {
     FSVD_HD int lo(int c, int G) const {
         if (c <= 0) return 0;
         if (c >= G) return total;
-        const int U = static_cast<int>(static_cast<unsigned long long>(total) * static_cast<unsigned>(c) / static_cast<unsigned>(G));
+        const int U = static_cast<int>(static_cast<unsigned>(total) * static_cast<unsigned>(c) / static_cast<unsigned>(G));
         if (exact) return U;
         int a, e;
         tile_span(tile_of(U), a, e);
@@ -193,7 +193,7 @@ struct MkSplit {
     }
     // CTA owning unit U (non-empty range)
     FSVD_HD int cta_of(int U, int G) const {
-        int c = static_cast<int>(static_cast<unsigned long long>(U) * static_cast<unsigned>(G) / static_cast<unsigned>(total));
+        int c = static_cast<int>(static_cast<unsigned>(U) * static_cast<unsigned>(G) / static_cast<unsigned>(total));
         if (c >= G) c = G - 1;
         while (c + 1 < G && lo(c + 1, G) <= U) ++c;
         while (c > 0 && lo(c, G) > U) --c;
@@ -312,15 +312,16 @@ struct ChunkSeq {
     }
 };
 
-// Same split over a plain row space (attention: B*H*len key rows).
-// (64-bit products: B * H * len * G can exceed 2^32 at long contexts)
+// Same split over a plain row space (attention: B*H*len key rows). 32-bit
+// products on purpose (64-bit divides are emulated and measured 16% slower on
+// the decode step); Session rejects shapes with B*H*capacity*grid >= 2^32.
 struct RowSplit {
     int total;
     FSVD_HD int lo(int c, int G) const {
-        return static_cast<int>(static_cast<unsigned long long>(total) * static_cast<unsigned>(c) / static_cast<unsigned>(G));
+        return static_cast<int>(static_cast<unsigned>(total) * static_cast<unsigned>(c) / static_cast<unsigned>(G));
     }
     FSVD_HD int cta_of(int U, int G) const {
-        int c = static_cast<int>(static_cast<unsigned long long>(U) * static_cast<unsigned>(G) / static_cast<unsigned>(total));
+        int c = static_cast<int>(static_cast<unsigned>(U) * static_cast<unsigned>(G) / static_cast<unsigned>(total));
         if (c >= G) c = G - 1;
         while (c + 1 < G && lo(c + 1, G) <= U) ++c;
         while (c > 0 && lo(c, G) > U) --c;

@@ -823,6 +823,9 @@ void Session::init(const fsvd_session_opts& o) {
         dec_splits_ = k::attn_decode_splits(B_, static_cast<int>(H), static_cast<int>(cap_));
         dec_part_ = static_cast<float*>(dalloc(4ull * B_ * H * dec_splits_ * (dh + 2)));
     } else {
+        // the megakernel's work splits multiply in 32 bits (decode_mk_common.cuh RowSplit / MkSplit)
+        if (static_cast<unsigned long long>(B_) * H * cap_ * mk_grid_ >= (1ull << 32))
+            throw ConfigError("decode megakernel: batch x heads x capacity x grid must stay below 2^32");
         attn_part_ = static_cast<float*>(dalloc(4ull * B_ * H * mk_splits_ * (dh + 2)));
         attn_count_ = static_cast<unsigned*>(dalloc(4ull * B_ * H));
         build_program();
