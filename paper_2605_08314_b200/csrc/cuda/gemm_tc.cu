@@ -37,9 +37,9 @@ constexpr int BM = 128, BK = 64;
 constexpr int kABytes = BM * 128;  // 16 KiB: 128 rows x 128 B
 constexpr int kThreads = 192;
 
-template <int BN, int BMT = 1>
+template <int BN, int BMT = 1, int CG = 1>
 struct Cfg {
-    static constexpr int kBBytes = BN * 128;
+    static constexpr int kBBytes = BN / CG * 128;  // a CTA pair holds half of the W tile in each CTA
     static constexpr int kStageBytes = BMT * kABytes + kBBytes;
     static constexpr int kStages = (200 * 1024) / kStageBytes;
     static constexpr int kSmem = kStages * kStageBytes + 1024 /*align*/ + 256 /*barriers*/;
@@ -52,6 +52,7 @@ struct TcArgs {
     GemmArgs g;
     int seg_tiles[3];  // BN-wide output tiles per segment
     int splits;        // split-K factor (blockIdx.z = split; > 1 only for kGemmStore / kGemmAddF32)
+    int cred;          // 1: the splits of a tile form one thread-block cluster and reduce through DSMEM
     int dbg;           // development: bit 0 = skip the MMAs (operand-stream-only timing)
 };
 
@@ -91,6 +92,43 @@ __device__ __forceinline__ void tma_load_2d(void* dst, const CUtensorMap* map, u
         "l"(map), "r"(smem_u32(bar)), "r"(c0), "r"(c1)
         : "memory");
 }
+// CTA-pair forms: the destination is this CTA's shared memory, the mbarrier the
+// leader CTA's (cta_group::2 lets the completion land in the peer of the pair)
+__device__ __forceinline__ void tma_load_4d_cg2(void* dst, const CUtensorMap* map, uint32_t bar_cluster, int c0,
+                                                int c1, int c2, int c3) {
+    asm volatile(
+        "cp.async.bulk.tensor.4d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%3, %4, "
+        "%5, %6}], [%2];" ::"r"(smem_u32(dst)),
+        "l"(map), "r"(bar_cluster), "r"(c0), "r"(c1), "r"(c2), "r"(c3)
+        : "memory");
+}
+__device__ __forceinline__ void tma_load_2d_cg2(void* dst, const CUtensorMap* map, uint32_t bar_cluster, int c0,
+                                                int c1) {
+    asm volatile(
+        "cp.async.bulk.tensor.2d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%3, "
+        "%4}], [%2];" ::"r"(smem_u32(dst)),
+        "l"(map), "r"(bar_cluster), "r"(c0), "r"(c1)
+        : "memory");
+}
+// shared::cluster address of the same object in CTA `rank` of the cluster
+__device__ __forceinline__ uint32_t mapa_u32(const void* p, uint32_t rank) {
+    uint32_t r;
+    asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(r) : "r"(smem_u32(p)), "r"(rank));
+    return r;
+}
+__device__ __forceinline__ uint32_t cluster_ctarank() {
+    uint32_t r;
+    asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
+    return r;
+}
+__device__ __forceinline__ float ld_cluster_f32(uint32_t addr) {
+    float v;
+    asm volatile("ld.shared::cluster.f32 %0, [%1];" : "=f"(v) : "r"(addr) : "memory");
+    return v;
+}
+__device__ __forceinline__ void cluster_sync_all() {
+    asm volatile("barrier.cluster.arrive.release.aligned;\nbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+}
 __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
     asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
                      smem_u32(dst)),
@@ -102,6 +140,25 @@ __device__ __forceinline__ void tc_fence_before() { asm volatile("tcgen05.fence:
 __device__ __forceinline__ void tc_commit(uint64_t* bar) {
     asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(smem_u32(bar))
                  : "memory");
+}
+// completion of the pair's MMAs -> the same mbarrier in both CTAs of the pair
+__device__ __forceinline__ void tc_commit_pair(uint64_t* bar, uint16_t mask) {
+    asm volatile(
+        "tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], %1;" ::"r"(
+            smem_u32(bar)),
+        "h"(mask)
+        : "memory");
+}
+// CTA pair: D[tmem of both CTAs] (+)= A[rows 0-127 in CTA 0, 128-255 in CTA 1] .
+// B[half of the N rows in each CTA]^T; issued by the leader CTA only
+__device__ __forceinline__ void tc_mma_pair(uint32_t tmem_d, uint64_t da, uint64_t db, uint32_t idesc, uint32_t accum) {
+    asm volatile(
+        "{\n"
+        ".reg .pred p;\n"
+        "setp.ne.b32 p, %4, 0;\n"
+        "tcgen05.mma.cta_group::2.kind::f16 [%0], %1, %2, %3, p;\n"
+        "}\n" ::"r"(tmem_d),
+        "l"(da), "l"(db), "r"(idesc), "r"(accum));
 }
 // D[tmem] (+)= A[smem] . B[smem]^T, bf16 in, fp32 accumulate
 __device__ __forceinline__ void tc_mma(uint32_t tmem_d, uint64_t da, uint64_t db, uint32_t idesc, uint32_t accum) {
@@ -125,10 +182,10 @@ __device__ __forceinline__ uint64_t sw128_desc(uint32_t saddr) {
     return d;
 }
 // instruction descriptor, kind::f16: D f32, A/B bf16, both K-major
-template <int N>
+template <int N, int MM = BM>
 __device__ __forceinline__ constexpr uint32_t idesc_bf16() {
     return (1u << 4) | (1u << 7) | (1u << 10) | (static_cast<uint32_t>(N >> 3) << 17) |
-           (static_cast<uint32_t>(BM >> 4) << 24);
+           (static_cast<uint32_t>(MM >> 4) << 24);
 }
 __device__ __forceinline__ void tmem_ld32(uint32_t taddr, float (&v)[32]) {
     uint32_t r[32];
@@ -167,10 +224,17 @@ __device__ __forceinline__ void store_bf16x32(__nv_bfloat16* dst, const float (&
 // -------------------------------------------------------------- kernel ----
 // BMT = 128-row M sub-tiles per CTA sharing each W tile (2: a 256 x BN tile in
 // two TMEM accumulators -- half the W traffic per FLOP of BMT = 1).
-template <int BN, bool DUAL, int BMT>
+//
+// CG = 2: a CTA pair (cluster of 2 on one TPC) computes a (CG*128*BMT) x BN tile
+// with tcgen05.mma.cta_group::2 (M = 256): each CTA loads its own 128-row X
+// sub-tiles and HALF of the W tile, the leader CTA issues the MMAs for both and
+// each CTA's TMEM holds its own rows' accumulators -- half the W bytes per SM
+// of CG = 1 at the same per-SM tile and MMA time.
+template <int BN, bool DUAL, int BMT, int CG>
 __global__ void __launch_bounds__(kThreads, 1) gemm_tc_kernel(const __grid_constant__ TcArgs A) {
     static_assert(!(DUAL && BMT > 1), "the dual GEMM uses the second accumulator for the gate");
-    using C = Cfg<BN, BMT>;
+    static_assert(CG == 1 || (BN / CG) % 16 == 0, "pair halves of the W tile are whole 16-row core-matrix groups");
+    using C = Cfg<BN, BMT, CG>;
     extern __shared__ __align__(1024) uint8_t smem_raw[];
     uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
     uint64_t* full = reinterpret_cast<uint64_t*>(smem + C::kStages * C::kStageBytes);
@@ -189,7 +253,12 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_tc_kernel(const __grid_const
         }
     }
     const GemvSeg& sg = g.seg[s];
-    const int n0 = tile * BN, m0 = blockIdx.x * BM * BMT;
+    // cluster rank = x + CG z (x: CTA of the pair, z: K split when the splits share a cluster)
+    const uint32_t crank = (CG == 2 || A.cred) ? cluster_ctarank() : 0u;
+    const uint32_t rank = crank % CG, lead = crank - rank;  // pair rank, the pair leader's cluster rank
+    const bool leader = rank == 0;
+    // rows of M sub-tile mi held by this CTA: pair base + mi * (CG * 128) + rank * 128
+    const int n0 = tile * BN, m0 = (blockIdx.x / CG) * BM * BMT * CG + static_cast<int>(rank) * BM;
     constexpr int kAcc = DUAL ? 2 : 1;
     constexpr uint32_t kAccStride = 256;  // dual: gate accumulator at TMEM column 256
     constexpr uint32_t kCols = (DUAL || BMT > 1) ? 2 * kAccStride : BN;
@@ -205,17 +274,90 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_tc_kernel(const __grid_const
         asm volatile("prefetch.tensormap [%0];" ::"l"(&A.xmap) : "memory");
     }
     if (warp == 0) {
-        asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_slot)),
-                     "r"(kAllocCols));
-        asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+        if constexpr (CG == 2) {
+            asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
+                             smem_u32(tmem_slot)),
+                         "r"(kAllocCols));
+            asm volatile("tcgen05.relinquish_alloc_permit.cta_group::2.sync.aligned;");
+        } else {
+            asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
+                             smem_u32(tmem_slot)),
+                         "r"(kAllocCols));
+            asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+        }
     }
     tc_fence_before();
-    __syncthreads();
+    if constexpr (CG == 2)
+        cluster_sync_all();  // both CTAs' barriers initialised before any TMA / commit crosses the pair
+    else
+        __syncthreads();
     tc_fence_after();
     const uint32_t tmem_base = *tmem_slot;
 
     // K-loop of accumulator j: segment, x column offset, k-blocks
     auto seg_of = [&](int j) -> const GemvSeg& { return DUAL ? g.seg[j] : sg; };
+    // fused epilogue of one 32-column chunk of output row t (columns n0 + c0 ..)
+    auto emit = [&](int t, int c0, float (&v)[32]) {
+        const int n = n0 + c0;
+        const int valid = min(32, sg.rows - n);
+        if (t >= g.M || valid <= 0) return;
+        if constexpr (DUAL) {  // v = silu(gate) * up already
+            store_bf16x32(static_cast<__nv_bfloat16*>(g.y) + static_cast<long long>(t) * g.y_ld + sg.y_off + n, v,
+                          valid);
+        } else if (A.splits > 1 && !A.cred) {  // fp32 partial of this K split (plain store / residual add)
+            float* w = g.ws + (static_cast<size_t>(blockIdx.z) * g.M + t) * g.y_ld + sg.y_off + n;
+            if (valid == 32 && (reinterpret_cast<uintptr_t>(w) & 15) == 0) {  // whole sectors
+#pragma unroll
+                for (int i = 0; i < 32; i += 4)
+                    __stcs(reinterpret_cast<float4*>(w + i), make_float4(v[i], v[i + 1], v[i + 2], v[i + 3]));
+            } else {
+#pragma unroll
+                for (int i = 0; i < 32; ++i)
+                    if (i < valid) w[i] = v[i];
+            }
+        } else if (g.epi == kGemmStore) {
+            store_bf16x32(static_cast<__nv_bfloat16*>(g.y) + static_cast<long long>(t) * g.y_ld + sg.y_off + n, v,
+                          valid);
+        } else if (g.epi == kGemmAddF32) {
+            float* y = static_cast<float*>(g.y) + static_cast<long long>(t) * g.y_ld + sg.y_off + n;
+            if (valid == 32 && (reinterpret_cast<uintptr_t>(y) & 15) == 0) {  // whole sectors
+                float4 r[8];
+#pragma unroll
+                for (int i = 0; i < 8; ++i) r[i] = reinterpret_cast<const float4*>(y)[i];
+#pragma unroll
+                for (int i = 0; i < 8; ++i)
+                    reinterpret_cast<float4*>(y)[i] = make_float4(r[i].x + v[4 * i], r[i].y + v[4 * i + 1],
+                                                                  r[i].z + v[4 * i + 2], r[i].w + v[4 * i + 3]);
+            } else {
+#pragma unroll
+                for (int i = 0; i < 32; ++i)
+                    if (i < valid) y[i] += v[i];
+            }
+        } else {  // kGemmQKV: RoPE (interleaved pairs, math.hpp:30-44) + q store / KV append
+            const int b = t / g.T, pos = (g.p0_dev ? *g.p0_dev : g.p0) + t % g.T;
+            if (sg.epi != kEpiV) {
+                const float2* cs = g.rope + static_cast<long long>(pos) * (g.d_head / 2);
+#pragma unroll
+                for (int i = 0; i < 32; i += 2) {
+                    const int ih = (n + i) % g.d_head;
+                    const float2 c = cs[ih >> 1];
+                    const float x0 = v[i], x1 = v[i + 1];
+                    v[i] = __fsub_rn(__fmul_rn(x0, c.x), __fmul_rn(x1, c.y));
+                    v[i + 1] = __fadd_rn(__fmul_rn(x0, c.y), __fmul_rn(x1, c.x));
+                }
+            }
+            if (sg.epi == kEpiRopeQ) {
+                store_bf16x32(static_cast<__nv_bfloat16*>(g.y) + static_cast<long long>(t) * g.y_ld + sg.y_off + n,
+                              v, valid);
+            } else {
+                const int h = n / g.d_head, ih = n % g.d_head;
+                __nv_bfloat16* c = static_cast<__nv_bfloat16*>(sg.epi == kEpiRopeK ? g.kcache : g.vcache);
+                store_bf16x32(c + b * g.cache_bstride + h * g.cache_hstride + static_cast<long long>(pos) * g.d_head +
+                                  ih,
+                              v, valid);
+            }
+        }
+    };
 
     // Programmatic dependent launch: this grid may start while the previous
     // kernel drains. Only the weight tiles (constant) are read before
@@ -228,19 +370,40 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_tc_kernel(const __grid_const
                 kb0 = nk * static_cast<int>(blockIdx.z) / A.splits;
                 kb1 = nk * (static_cast<int>(blockIdx.z) + 1) / A.splits;
             };
-            const int t0 = n0 / 16;
-            // the W box always lands whole (tiles past the end are zero-filled)
-            const uint32_t bytes = BMT * kABytes + static_cast<uint32_t>(BN / 16) * kLineTileBytes;
+            // development (dbg bit 1): rotate each CTA's k-block order by its N tile
+            auto kk = [&](int kb, int kb0, int kb1) {
+                if (!(A.dbg & 2)) return kb;
+                const int n = kb1 - kb0;
+                return kb0 + (kb - kb0 + static_cast<int>(blockIdx.y) * 5) % n;
+            };
+            const int t0 = n0 / 16 + static_cast<int>(rank) * (BN / CG / 16);  // this CTA's half of the W tile
+            // the W box always lands whole (tiles past the end are zero-filled); the
+            // leader's full barrier counts the bytes of both CTAs of a pair
+            const uint32_t bytes = CG * (BMT * kABytes + static_cast<uint32_t>(BN / CG / 16) * kLineTileBytes);
+            auto load_w = [&](int st, const CUtensorMap* wm, int kb) {
+                uint8_t* dst = smem + st * C::kStageBytes + BMT * kABytes;
+                if constexpr (CG == 2) {
+                    if (leader) mbar_expect_tx(&full[st], bytes);
+                    tma_load_4d_cg2(dst, wm, mapa_u32(&full[st], lead), 0, 0, kb, t0);
+                } else {
+                    mbar_expect_tx(&full[st], bytes);
+                    tma_load_4d(dst, wm, &full[st], 0, 0, kb, t0);
+                }
+            };
+            auto load_x = [&](int st, int mi, int kcol) {
+                uint8_t* dst = smem + st * C::kStageBytes + mi * kABytes;
+                if constexpr (CG == 2)
+                    tma_load_2d_cg2(dst, &A.xmap, mapa_u32(&full[st], lead), kcol, m0 + mi * BM * CG);
+                else
+                    tma_load_2d(dst, &A.xmap, &full[st], kcol, m0 + mi * BM);
+            };
             // W tiles of the first ring round, ahead of the grid dependency
             int npre = 0;
             for (int j = 0; j < kAcc && npre < C::kStages; ++j) {
                 int kb0, kb1;
                 kb_range(j, kb0, kb1);
-                for (int kb = kb0; kb < kb1 && npre < C::kStages; ++kb, ++npre) {
-                    mbar_expect_tx(&full[npre], bytes);
-                    tma_load_4d(smem + npre * C::kStageBytes + BMT * kABytes, &A.wmap[DUAL ? j : s], &full[npre], 0,
-                                0, kb, t0);
-                }
+                for (int kb = kb0; kb < kb1 && npre < C::kStages; ++kb, ++npre)
+                    load_w(npre, &A.wmap[DUAL ? j : s], kk(kb, kb0, kb1));
             }
             asm volatile("griddepcontrol.wait;" ::: "memory");
             int it = 0;
@@ -254,21 +417,18 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_tc_kernel(const __grid_const
                 for (int kb = kb0; kb < kb1; ++kb, ++it) {
                     const int st = it % C::kStages;
                     const uint32_t ph = (it / C::kStages) & 1;
-                    uint8_t* sa = smem + st * C::kStageBytes;
                     if (it >= npre) {
                         mbar_wait(&empty[st], ph ^ 1);
-                        mbar_expect_tx(&full[st], bytes);
-                        tma_load_4d(sa + BMT * kABytes, wm, &full[st], 0, 0, kb, t0);
+                        load_w(st, wm, kk(kb, kb0, kb1));
                     }
 #pragma unroll
-                    for (int mi = 0; mi < BMT; ++mi)
-                        tma_load_2d(sa + mi * kABytes, &A.xmap, &full[st], sj.x_off + kb * BK, m0 + mi * BM);
+                    for (int mi = 0; mi < BMT; ++mi) load_x(st, mi, sj.x_off + kk(kb, kb0, kb1) * BK);
                 }
             }
         }
     } else if (warp == 1) {
-        if (lane == 0) {
-            constexpr uint32_t idesc = idesc_bf16<BN>();
+        if (lane == 0 && leader) {
+            constexpr uint32_t idesc = idesc_bf16<BN, BM * CG>();
             int it = 0;
 #pragma unroll 1
             for (int j = 0; j < kAcc; ++j) {
@@ -290,15 +450,26 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_tc_kernel(const __grid_const
                         for (int mi = 0; mi < BMT; ++mi) {
                             const uint64_t da = sw128_desc(sa + mi * kABytes);
 #pragma unroll
-                            for (int k = 0; k < BK / 16; ++k)  // +32 B per K=16 step inside the 128 B swizzle atom
-                                tc_mma(tacc + mi * kAccStride, da + 2 * k, db + 2 * k, idesc,
-                                       (kb != kb0 || k != 0) ? 1u : 0u);
+                            for (int k = 0; k < BK / 16; ++k) {  // +32 B per K=16 step inside the 128 B swizzle atom
+                                if constexpr (CG == 2)
+                                    tc_mma_pair(tacc + mi * kAccStride, da + 2 * k, db + 2 * k, idesc,
+                                                (kb != kb0 || k != 0) ? 1u : 0u);
+                                else
+                                    tc_mma(tacc + mi * kAccStride, da + 2 * k, db + 2 * k, idesc,
+                                           (kb != kb0 || k != 0) ? 1u : 0u);
+                            }
                         }
                     }
-                    tc_commit(&empty[st]);
+                    if constexpr (CG == 2)
+                        tc_commit_pair(&empty[st], static_cast<uint16_t>(3u << lead));
+                    else
+                        tc_commit(&empty[st]);
                 }
             }
-            tc_commit(tmem_full);
+            if constexpr (CG == 2)
+                tc_commit_pair(tmem_full, static_cast<uint16_t>(3u << lead));
+            else
+                tc_commit(tmem_full);
         }
     } else {
         // epilogue: warp w reads TMEM lanes 32*(w%4) .. +31 (= tile rows)
@@ -307,83 +478,76 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_tc_kernel(const __grid_const
         asm volatile("griddepcontrol.wait;" ::: "memory");
         mbar_wait(tmem_full, 0);
         tc_fence_after();
+        if (!DUAL && A.cred) {
+            // cluster split-K: this split's fp32 partial -> own smem as [column][row]
+            // (the ring is idle: every MMA that read it has completed)
+            float* red = reinterpret_cast<float*>(smem);
+            const uint32_t lane_addr = tmem_base + (static_cast<uint32_t>(q * 32) << 16);
 #pragma unroll 1
-        for (int mi = 0; mi < BMT; ++mi)
-#pragma unroll 1
-        for (int c0 = 0; c0 < BN; c0 += 32) {
-            const int t = m0 + mi * BM + row;
-            const uint32_t lane_addr = tmem_base + (static_cast<uint32_t>(q * 32) << 16) + mi * kAccStride;
-            float v[32], gt[32];
-            tmem_ld32(lane_addr + c0, v);  // .sync.aligned: every lane, before any divergence
-            if constexpr (DUAL) tmem_ld32(lane_addr + kAccStride + c0, gt);
-            const int n = n0 + c0;
-            const int valid = min(32, sg.rows - n);
-            if (t >= g.M || valid <= 0) continue;
-            if constexpr (DUAL) {
+            for (int c0 = 0; c0 < BN; c0 += 32) {
+                float v[32];
+                tmem_ld32(lane_addr + c0, v);
 #pragma unroll
-                for (int i = 0; i < 32; ++i) v[i] = silu_mul(gt[i], v[i]);
-                store_bf16x32(static_cast<__nv_bfloat16*>(g.y) + static_cast<long long>(t) * g.y_ld + sg.y_off + n, v,
-                              valid);
-            } else if (A.splits > 1) {  // fp32 partial of this K split (plain store / residual add)
-                float* w = g.ws + (static_cast<size_t>(blockIdx.z) * g.M + t) * g.y_ld + sg.y_off + n;
-                if (valid == 32 && (reinterpret_cast<uintptr_t>(w) & 15) == 0) {  // whole sectors
-#pragma unroll
-                    for (int i = 0; i < 32; i += 4)
-                        __stcs(reinterpret_cast<float4*>(w + i), make_float4(v[i], v[i + 1], v[i + 2], v[i + 3]));
-                } else {
-#pragma unroll
-                    for (int i = 0; i < 32; ++i)
-                        if (i < valid) w[i] = v[i];
-                }
-            } else if (g.epi == kGemmStore) {
-                store_bf16x32(static_cast<__nv_bfloat16*>(g.y) + static_cast<long long>(t) * g.y_ld + sg.y_off + n, v,
-                              valid);
-            } else if (g.epi == kGemmAddF32) {
-                float* y = static_cast<float*>(g.y) + static_cast<long long>(t) * g.y_ld + sg.y_off + n;
-                if (valid == 32 && (reinterpret_cast<uintptr_t>(y) & 15) == 0) {  // whole sectors
-                    float4 r[8];
-#pragma unroll
-                    for (int i = 0; i < 8; ++i) r[i] = reinterpret_cast<const float4*>(y)[i];
-#pragma unroll
-                    for (int i = 0; i < 8; ++i)
-                        reinterpret_cast<float4*>(y)[i] = make_float4(r[i].x + v[4 * i], r[i].y + v[4 * i + 1],
-                                                                      r[i].z + v[4 * i + 2], r[i].w + v[4 * i + 3]);
-                } else {
-#pragma unroll
-                    for (int i = 0; i < 32; ++i)
-                        if (i < valid) y[i] += v[i];
-                }
-            } else {  // kGemmQKV: RoPE (interleaved pairs, math.hpp:30-44) + q store / KV append
-                const int b = t / g.T, pos = (g.p0_dev ? *g.p0_dev : g.p0) + t % g.T;
-                if (sg.epi != kEpiV) {
-                    const float2* cs = g.rope + static_cast<long long>(pos) * (g.d_head / 2);
-#pragma unroll
-                    for (int i = 0; i < 32; i += 2) {
-                        const int ih = (n + i) % g.d_head;
-                        const float2 c = cs[ih >> 1];
-                        const float x0 = v[i], x1 = v[i + 1];
-                        v[i] = __fsub_rn(__fmul_rn(x0, c.x), __fmul_rn(x1, c.y));
-                        v[i + 1] = __fadd_rn(__fmul_rn(x0, c.y), __fmul_rn(x1, c.x));
-                    }
-                }
-                if (sg.epi == kEpiRopeQ) {
-                    store_bf16x32(static_cast<__nv_bfloat16*>(g.y) + static_cast<long long>(t) * g.y_ld + sg.y_off + n,
-                                  v, valid);
-                } else {
-                    const int h = n / g.d_head, ih = n % g.d_head;
-                    __nv_bfloat16* c = static_cast<__nv_bfloat16*>(sg.epi == kEpiRopeK ? g.kcache : g.vcache);
-                    store_bf16x32(c + b * g.cache_bstride + h * g.cache_hstride + static_cast<long long>(pos) * g.d_head +
-                                      ih,
-                                  v, valid);
-                }
+                for (int i = 0; i < 32; ++i) red[(c0 + i) * BM + row] = v[i];
             }
+        } else {
+#pragma unroll 1
+            for (int mi = 0; mi < BMT; ++mi)
+#pragma unroll 1
+                for (int c0 = 0; c0 < BN; c0 += 32) {
+                    const uint32_t lane_addr = tmem_base + (static_cast<uint32_t>(q * 32) << 16) + mi * kAccStride;
+                    float v[32], gt[32];
+                    tmem_ld32(lane_addr + c0, v);  // .sync.aligned: every lane, before any divergence
+                    if constexpr (DUAL) tmem_ld32(lane_addr + kAccStride + c0, gt);
+                    if constexpr (DUAL) {
+#pragma unroll
+                        for (int i = 0; i < 32; ++i) v[i] = silu_mul(gt[i], v[i]);
+                    }
+                    emit(m0 + mi * BM * CG + row, c0, v);
+                }
         }
     }
     tc_fence_before();
-    __syncthreads();
+    if constexpr (CG == 2)
+        cluster_sync_all();  // the leader's MMAs write the peer's TMEM and commit to its barriers
+    else
+        __syncthreads();
+    if (!DUAL && A.cred) {
+        // The S = splits CTAs holding partials of the same rows (cluster ranks
+        // x + CG z, z = split) reduce them through DSMEM: split z owns the column
+        // slice [z BN/S, (z+1) BN/S), sums the S partials in split order and runs
+        // the fused epilogue on it.
+        if constexpr (CG == 1) cluster_sync_all();
+        if (warp >= 2) {
+            const int S = A.splits, cols = BN / S;
+            const int z = static_cast<int>(blockIdx.z), row = (warp & 3) * 32 + lane;
+            const uint32_t base = smem_u32(smem);
+#pragma unroll 1
+            for (int c0 = z * cols; c0 < (z + 1) * cols; c0 += 32) {
+                float v[32];
+#pragma unroll 1
+                for (int zz = 0; zz < S; ++zz) {
+                    uint32_t a;
+                    asm volatile("mapa.shared::cluster.u32 %0, %1, %2;"
+                                 : "=r"(a)
+                                 : "r"(base + static_cast<uint32_t>(c0 * BM + row) * 4u), "r"(rank + CG * zz));  // same pair half, split zz
+#pragma unroll
+                    for (int i = 0; i < 32; ++i) {
+                        const float pv = ld_cluster_f32(a + i * BM * 4);
+                        v[i] = zz == 0 ? pv : v[i] + pv;
+                    }
+                }
+                emit(m0 + row, c0, v);
+            }
+        }
+        cluster_sync_all();  // peers have read this CTA's partial
+    }
     if (warp == 0) {
         tc_fence_after();
-        asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem_base), "r"(kAllocCols));
+        if constexpr (CG == 2)
+            asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, %1;" ::"r"(tmem_base), "r"(kAllocCols));
+        else
+            asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem_base), "r"(kAllocCols));
     }
 }
 
@@ -541,7 +705,13 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_swap_kernel(const __grid_con
         if constexpr (DUAL) tmem_ld_cols<NT>(lane_addr + kGateCol, gt);
         const bool ok = n < sg.rows;
         const int M = g.M;
-        if constexpr (DUAL) {
+        if (!DUAL && A.cred) {
+            // cluster split-K: this split's fp32 partial -> own smem as [token][row]
+            // (the ring is idle: every MMA that read it has completed)
+            float* red = reinterpret_cast<float*>(smem);
+#pragma unroll
+            for (int t = 0; t < NT; ++t) red[t * kSwapRows + q * 32 + lane] = v[t];
+        } else if constexpr (DUAL) {
             if (ok)
 #pragma unroll
                 for (int t = 0; t < NT; ++t)
@@ -594,6 +764,38 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_swap_kernel(const __grid_con
     }
     tc_fence_before();
     __syncthreads();
+    if (!DUAL && A.cred) {
+        // The S = splits CTAs of this output tile are one cluster (rank = split).
+        // CTA z reduces rows [z R, z R + R) of the tile over all S partials, in
+        // split order, straight from the peers' shared memory, and writes them.
+        cluster_sync_all();
+        if (warp >= 2) {
+            const int S = A.splits, R = kSwapRows / S;
+            const uint32_t z = cluster_ctarank();
+            const int idx = threadIdx.x - 64, r = static_cast<int>(z) * R + idx % R, tg = idx / R;
+            const int n = n0 + r;
+            const bool ok = n < sg.rows;
+            const uint32_t base = smem_u32(smem);
+#pragma unroll 1
+            for (int t = tg; t < NT; t += S) {
+                const uint32_t off = static_cast<uint32_t>(t * kSwapRows + r) * 4u;
+                float acc = 0.f;
+                for (int zz = 0; zz < S; ++zz) {
+                    uint32_t a;
+                    asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(a) : "r"(base + off), "r"(zz));
+                    const float pv = ld_cluster_f32(a);
+                    acc = zz == 0 ? pv : acc + pv;
+                }
+                if (!ok || t >= g.M) continue;
+                const long long o = static_cast<long long>(t) * g.y_ld + sg.y_off + n;
+                if (g.epi == kGemmAddF32)
+                    static_cast<float*>(g.y)[o] += acc;
+                else
+                    static_cast<__nv_bfloat16*>(g.y)[o] = __float2bfloat16_rn(acc);
+            }
+        }
+        cluster_sync_all();  // peers have read this CTA's partial
+    }
     if (warp == 0) {
         tc_fence_after();
         asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem_base), "r"(kAllocCols));
@@ -610,7 +812,25 @@ void launch_swap(const TcArgs& ta, int tiles, cudaStream_t s) {
         cudaFuncSetAttribute(gemm_swap_kernel<NT, DUAL>, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmem);
         attr = true;
     }
-    launch_pdl(gemm_swap_kernel<NT, DUAL>, dim3(1, tiles, ta.splits), dim3(kThreads), kSmem, s, ta);
+    if (!ta.cred) {
+        launch_pdl(gemm_swap_kernel<NT, DUAL>, dim3(1, tiles, ta.splits), dim3(kThreads), kSmem, s, ta);
+        return;
+    }
+    cudaLaunchConfig_t cfg{};
+    cfg.gridDim = dim3(1, tiles, ta.splits);
+    cfg.blockDim = dim3(kThreads);
+    cfg.dynamicSmemBytes = kSmem;
+    cfg.stream = s;
+    cudaLaunchAttribute at[2];
+    at[0].id = cudaLaunchAttributeClusterDimension;
+    at[0].val.clusterDim.x = 1;
+    at[0].val.clusterDim.y = 1;
+    at[0].val.clusterDim.z = ta.splits;
+    at[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    at[1].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = at;
+    cfg.numAttrs = std::getenv("FSVD_NO_PDL") ? 1 : 2;
+    cudaLaunchKernelEx(&cfg, gemm_swap_kernel<NT, DUAL>, ta);
 }
 
 // ------------------------------------------------------------ host side ----
@@ -660,27 +880,38 @@ __global__ void __launch_bounds__(256) splitk_reduce_kernel(const __grid_constan
     }
 }
 
-template <int BN, bool DUAL, int BMT>
+template <int BN, bool DUAL, int BMT, int CG = 1>
 void launch(const TcArgs& ta, int tiles, int M, cudaStream_t s) {
-    using C = Cfg<BN, BMT>;
+    using C = Cfg<BN, BMT, CG>;
     static bool attr = false;
     if (!attr) {
-        cudaFuncSetAttribute(gemm_tc_kernel<BN, DUAL, BMT>, cudaFuncAttributeMaxDynamicSharedMemorySize, C::kSmem);
+        cudaFuncSetAttribute(gemm_tc_kernel<BN, DUAL, BMT, CG>, cudaFuncAttributeMaxDynamicSharedMemorySize, C::kSmem);
         attr = true;
     }
-    dim3 grid((M + BM * BMT - 1) / (BM * BMT), tiles, ta.splits);
+    dim3 grid((M + BM * BMT * CG - 1) / (BM * BMT * CG) * CG, tiles, ta.splits);
     cudaLaunchConfig_t cfg{};
     cfg.gridDim = grid;
     cfg.blockDim = dim3(kThreads);
     cfg.dynamicSmemBytes = C::kSmem;
     cfg.stream = s;
-    cudaLaunchAttribute pdl[1];
-    pdl[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
-    pdl[0].val.programmaticStreamSerializationAllowed = 1;
-    cfg.attrs = pdl;
-    cfg.numAttrs = std::getenv("FSVD_NO_PDL") ? 0 : 1;
-    cudaLaunchKernelEx(&cfg, gemm_tc_kernel<BN, DUAL, BMT>, ta);
-    if (ta.splits > 1) {
+    cudaLaunchAttribute at[2];
+    int na = 0;
+    if (CG > 1 || ta.cred) {
+        at[na].id = cudaLaunchAttributeClusterDimension;
+        at[na].val.clusterDim.x = CG;
+        at[na].val.clusterDim.y = 1;
+        at[na].val.clusterDim.z = ta.cred ? ta.splits : 1;
+        ++na;
+    }
+    if (!std::getenv("FSVD_NO_PDL")) {
+        at[na].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+        at[na].val.programmaticStreamSerializationAllowed = 1;
+        ++na;
+    }
+    cfg.attrs = at;
+    cfg.numAttrs = na;
+    cudaLaunchKernelEx(&cfg, gemm_tc_kernel<BN, DUAL, BMT, CG>, ta);
+    if (ta.splits > 1 && !ta.cred) {
         int rows = 0;
         for (int i = 0; i < ta.g.nseg; ++i) rows = std::max(rows, ta.g.seg[i].rows);
         launch_pdl(splitk_reduce_kernel, dim3((rows + 255) / 256, M), dim3(256), 0, s, ta);
@@ -747,25 +978,28 @@ void gemm_tc(const GemmArgs& a, int x_rows, cudaStream_t s) {
             while (sp > 1 && static_cast<size_t>(sp) * a.M * a.y_ld > a.ws_floats) --sp;
         }
         if (const char* e = std::getenv("FSVD_GEMM_SPLITS"); e && can_split) sp = std::max(1, std::atoi(e));
+        // splits reduce in-kernel through DSMEM (one cluster per tile): a power of two <= 8
+        ta.cred = sp > 1 && !std::getenv("FSVD_NO_CRED");
+        if (ta.cred) sp = sp >= 8 ? 8 : sp >= 4 ? 4 : 2;
         for (int i = 0; i < nseg; ++i) ta.seg_tiles[i] = (a.seg[i].rows + kSwapRows - 1) / kSwapRows;
         for (int i = 0; i < a.nseg; ++i) encode_w(i, kSwapRows);
         ta.splits = sp;
         if (std::getenv("FSVD_GEMM_LOG"))
-            std::fprintf(stderr, "gemm_swap M=%d N0=%d nseg=%d nk=%d epi=%d -> NT=%d splits=%d tiles=%d\n", a.M,
-                         a.seg[0].rows, a.nseg, nk_max, a.epi, NT, sp, tiles);
+            std::fprintf(stderr, "gemm_swap M=%d N0=%d nseg=%d nk=%d epi=%d -> NT=%d splits=%d%s tiles=%d\n", a.M,
+                         a.seg[0].rows, a.nseg, nk_max, a.epi, NT, sp, ta.cred ? " (cluster)" : "", tiles);
         if (NT == 16) {
             if (dual) launch_swap<16, true>(ta, tiles, s); else launch_swap<16, false>(ta, tiles, s);
         } else {
             if (dual) launch_swap<32, true>(ta, tiles, s); else launch_swap<32, false>(ta, tiles, s);
         }
-        if (sp > 1) {
+        if (sp > 1 && !ta.cred) {
             int rows = 0;
             for (int i = 0; i < a.nseg; ++i) rows = std::max(rows, a.seg[i].rows);
             launch_pdl(splitk_reduce_kernel, dim3((rows + 255) / 256, a.M), dim3(256), 0, s, ta);
         }
         return;
     }
-    int best_bn = 128, best_sp = 1, best_bmt = 1;
+    int best_bn = 128, best_sp = 1, best_bmt = 1, best_cg = 1, best_cred = 0;
     if (a.M <= BM) {
         // Decode-sized M (batched engine): the weight stream is the whole cost and
         // the fp32 partials are tiny. Tile width and split-K factor from a wave
@@ -825,9 +1059,56 @@ void gemm_tc(const GemmArgs& a, int x_rows, cudaStream_t s) {
                 }
             }
     }
+    if (a.M > BM && a.M <= 1024 && !dual && !std::getenv("FSVD_NO_PAIR")) {
+        // Under-filled long-K projections (qkvA, oA, upgateA, downA at 512 tokens):
+        // 256 x 256 CTA-pair tiles, K split over the CTAs of one cluster and
+        // reduced through DSMEM (tools/gemm_sweep.cu cred512: 10-20 % faster
+        // than the best single-CTA tile at these shapes). S = 4 when that still
+        // fits one wave, else 2.
+        const int pairs = count_tiles(256) * ((a.M + 255) / 256);
+        if (a.epi == kGemmQKV) {  // RoPE / KV-append epilogue: pair tiles, no split (+2 % prefill)
+            best_bn = 256;
+            best_bmt = 1;
+            best_cg = 2;
+            best_sp = 1;
+        } else if (nk_min >= 32 && pairs * 2 <= 74) {
+            best_bn = 256;
+            best_bmt = 1;
+            best_cg = 2;
+            best_sp = pairs * 2 * 4 <= 148 ? 4 : 2;
+            best_cred = 1;
+        }
+    }
     if (const char* e = std::getenv("FSVD_GEMM_BN")) best_bn = std::atoi(e);
     if (const char* e = std::getenv("FSVD_GEMM_SPLITS"); e && can_split) best_sp = std::max(1, std::atoi(e));
     if (const char* e = std::getenv("FSVD_GEMM_BMT"); e && !dual) best_bmt = std::atoi(e) == 2 ? 2 : 1;
+    {  // development: per-epilogue override FSVD_GEMM_E<epi>=bn,bmt,splits
+        const std::string key = "FSVD_GEMM_E" + std::to_string(a.epi);
+        if (const char* e = std::getenv(key.c_str())) {
+            int bn = best_bn, bmt = best_bmt, sp = best_sp, cg = best_cg;
+            std::sscanf(e, "%d,%d,%d,%d", &bn, &bmt, &sp, &cg);
+            best_bn = bn;
+            best_bmt = dual ? 1 : (bmt == 2 ? 2 : 1);
+            best_sp = can_split ? std::max(1, sp) : 1;
+            best_cg = cg == 2 ? 2 : 1;
+        }
+    }
+    if (const char* e = std::getenv("FSVD_GEMM_CG")) best_cg = std::atoi(e) == 2 ? 2 : 1;
+    if (a.M <= BM) best_cg = 1;
+    // cluster split-K (partials reduced through DSMEM inside the kernel, any epilogue but
+    // the dual one): needs one 128-row accumulator, BN/S a multiple of 32, CG*S <= 8
+    int cred = best_cred;
+    if (const char* e = std::getenv("FSVD_GEMM_CRED")) cred = std::atoi(e);
+    if (const char* e = std::getenv(("FSVD_GEMM_E" + std::to_string(a.epi)).c_str())) {
+        int x[5] = {0, 0, 0, 0, cred};
+        std::sscanf(e, "%d,%d,%d,%d,%d", &x[0], &x[1], &x[2], &x[3], &x[4]);
+        cred = x[4];
+        if (cred && !dual) best_sp = std::max(1, x[2]);  // cluster splits need no workspace
+    }
+    if (cred && (dual || best_bmt != 1 || best_sp < 2 || (best_bn % (32 * best_sp)) != 0 || best_cg * best_sp > 8))
+        cred = 0;
+    if (!cred && !can_split) best_sp = 1;
+    ta.cred = cred;
     if (best_bmt == 2) best_bn = 256;
     if (const char* e = std::getenv("FSVD_GEMM_DBG")) ta.dbg = std::atoi(e);
     const int BN = best_bn;
@@ -837,13 +1118,28 @@ void gemm_tc(const GemmArgs& a, int x_rows, cudaStream_t s) {
         tiles += ta.seg_tiles[i];
     }
     ta.splits = best_sp;
-    for (int i = 0; i < a.nseg; ++i) encode_w(i, BN);
+    for (int i = 0; i < a.nseg; ++i) encode_w(i, BN / best_cg);  // a pair CTA loads half of the W tile
     if (std::getenv("FSVD_GEMM_LOG"))
-        std::fprintf(stderr, "gemm_tc M=%d N0=%d nseg=%d nk=%d epi=%d -> BN=%d BMT=%d splits=%d tiles=%d\n", a.M,
-                     a.seg[0].rows, a.nseg, nk_max, a.epi, BN, best_bmt, best_sp, tiles);
+        std::fprintf(stderr, "gemm_tc M=%d N0=%d nseg=%d nk=%d epi=%d -> BN=%d BMT=%d CG=%d splits=%d tiles=%d\n",
+                     a.M, a.seg[0].rows, a.nseg, nk_max, a.epi, BN, best_bmt, best_cg, best_sp, tiles);
     if (best_bmt == 2) {
-        launch<256, false, 2>(ta, tiles, a.M, s);
+        if (best_cg == 2)
+            launch<256, false, 2, 2>(ta, tiles, a.M, s);
+        else
+            launch<256, false, 2>(ta, tiles, a.M, s);
         return;
+    }
+    if (best_cg == 2) {
+#define FSVD_TC_BN2(N)                                   \
+    if (BN == N) {                                       \
+        if (dual)                                        \
+            launch<N, true, 1, 2>(ta, tiles, a.M, s);    \
+        else                                             \
+            launch<N, false, 1, 2>(ta, tiles, a.M, s);   \
+        return;                                          \
+    }
+        FSVD_TC_BN2(128) FSVD_TC_BN2(160) FSVD_TC_BN2(192) FSVD_TC_BN2(224) FSVD_TC_BN2(256)
+#undef FSVD_TC_BN2
     }
 #define FSVD_TC_BN(N)                                  \
     if (BN == N) {                                     \
