@@ -49,6 +49,7 @@ HOST_SOURCES = ["host/model.cpp", "host/checkpoint.cpp", "host/canonical.cpp", "
 CUDA_SOURCES = [
     "cuda/decode_mk.cu",
     "cuda/attention.cu",
+    "cuda/attn_tc.cu",
     "cuda/gemm_simt.cu",
     "cuda/gemm_tc.cu",
     "cuda/gemm.cu",

@@ -413,6 +413,7 @@ bool attn_decode(WType wt, const AttnPrefillArgs& a, float* part, int S, cudaStr
 }
 
 void attn_prefill(WType wt, const AttnPrefillArgs& a, cudaStream_t s) {
+    if (wt == kBF16 && attn_prefill_tcgen05(a, s)) return;
     if (wt == kBF16 && (a.d_head == 64 || a.d_head == 128) && a.q_ld % 8 == 0 && a.out_ld % 8 == 0) {
         dim3 grid((a.T + kFQ - 1) / kFQ, a.n_heads, a.batch);
         const int smem = (kFQ + 4 * kFK) * (a.d_head + 8) * 2;

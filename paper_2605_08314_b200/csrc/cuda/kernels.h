@@ -51,6 +51,8 @@ struct AttnPrefillArgs {
     const int* p0_dev;   // non-null: p0 = *p0_dev (graph-replayed batched decode)
 };
 void attn_prefill(WType wt, const AttnPrefillArgs& a, cudaStream_t s);
+// tcgen05/TMEM flash attention (attn_tc.cu, bf16, d_head 64 / 128); false if not covered
+bool attn_prefill_tcgen05(const AttnPrefillArgs& a, cudaStream_t s);
 // Split-KV flash decode (T = 1, bf16, d_head 128): partials [B][H][S][d_head + 2]
 // fp32 then an in-order merge; false if the shape is not covered.
 int attn_decode_splits(int batch, int n_heads, int capacity);
