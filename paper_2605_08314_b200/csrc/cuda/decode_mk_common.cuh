@@ -362,12 +362,19 @@ struct ChunkDot<__nv_bfloat16, B> {
         const int g = lane >> 2, t = lane & 3;
         const int r = (lane & 7) + 8 * ((lane >> 3) & 1);  // row this lane addresses for ldmatrix
         const int hi = lane >> 4;                          // which 16-B chunk of the k-step
-        const __nv_bfloat16* xp = x + g * x_len + kbase + 2 * t;
+        // the planes are k-permuted per 64-element line (plane_pos): lane t's B
+        // fragments of the line's four k-steps are 32 contiguous bytes
+        const __nv_bfloat16* xp = x + g * x_len + kbase + 16 * t;
         const uint32_t a_row = static_cast<uint32_t>(__cvta_generic_to_shared(buf)) + r * kLineBytes;
         float d[4][4] = {};
 #pragma unroll 2
         for (int l = 0; l < nl; ++l) {
             const uint32_t lrow = a_row + l * kLineTileBytes;
+            uint4 xb[2] = {make_uint4(0u, 0u, 0u, 0u), make_uint4(0u, 0u, 0u, 0u)};
+            if (g < 2 * B) {
+                xb[0] = *reinterpret_cast<const uint4*>(xp + l * 64);
+                xb[1] = *reinterpret_cast<const uint4*>(xp + l * 64 + 8);
+            }
 #pragma unroll
             for (int j = 0; j < 4; ++j) {
                 uint32_t a0, a1, a2, a3;
@@ -375,11 +382,8 @@ struct ChunkDot<__nv_bfloat16, B> {
                 asm volatile("ldmatrix.sync.aligned.m8n8.x4.shared.b16 {%0,%1,%2,%3}, [%4];"
                              : "=r"(a0), "=r"(a1), "=r"(a2), "=r"(a3)
                              : "r"(addr));
-                uint32_t b0 = 0u, b1 = 0u;
-                if (g < 2 * B) {
-                    b0 = *reinterpret_cast<const uint32_t*>(xp + l * 64 + 16 * j);
-                    b1 = *reinterpret_cast<const uint32_t*>(xp + l * 64 + 16 * j + 8);
-                }
+                const uint4& q = xb[j >> 1];
+                const uint32_t b0 = (j & 1) ? q.z : q.x, b1 = (j & 1) ? q.w : q.y;
                 mma_bf16(d[j], a0, a1, a2, a3, b0, b1);
             }
         }
@@ -430,11 +434,19 @@ struct PlaneIO;
 template <>
 struct PlaneIO<__nv_bfloat16> {
     static constexpr int kBytesPerElem = 4;  // hi + lo
+    // Element k of each 64-element line sits at 16 t + 4 j + w, where j = k / 16
+    // is the mma k-step, t = (k % 8) / 2 the lane quad index and w picks
+    // (2t, 2t+1, 2t+8, 2t+9): the B fragments lane t needs for the whole line.
+    static __device__ __forceinline__ int plane_pos(int i) {
+        const int k = i & 63, j = k >> 4, r = k & 15;
+        return (i & ~63) | (((r & 7) >> 1) << 4) | (j << 2) | (r & 1) | ((r & 8) >> 2);
+    }
     static __device__ __forceinline__ void put(const Planes& p, int b, int i, float v) {
         __nv_bfloat16* q = static_cast<__nv_bfloat16*>(p.p) + static_cast<size_t>(2 * b) * p.len;
         const __nv_bfloat16 h = __float2bfloat16_rn(v);
-        q[i] = h;
-        q[p.len + i] = __float2bfloat16_rn(v - __bfloat162float(h));
+        const int o = plane_pos(i);
+        q[o] = h;
+        q[p.len + o] = __float2bfloat16_rn(v - __bfloat162float(h));
     }
 };
 template <>

@@ -147,7 +147,7 @@ void allocate(DeviceModel& dm, const std::vector<std::array<size_t, kNumProj>>& 
         for (size_t p = 0; p < kNumProj; ++p) {
             const auto dims = proj_dims(c, p);
             L.r[p] = static_cast<int>(ranks[l][p]);
-            L.rp[p] = pad8(ranks[l][p]);
+            L.rp[p] = pad64(ranks[l][p]);  // 64: the decode planes' k-permutation groups (decode_mk_common.cuh)
             const void* key = keys[l][p];
             auto it = key ? shared.find(key) : shared.end();
             if (it != shared.end()) {
@@ -790,7 +790,7 @@ void Session::init(const fsvd_session_opts& o) {
     tokens_ = static_cast<int*>(dalloc(4 * B_));
 
     // rank-space vectors of the prefill path: segment s of a packed
-    // projection starts at the sum of the previous segments' pad8 ranks; the
+    // projection starts at the sum of the previous segments' pad64 ranks; the
     // stride covers the last segment's padded (tile-layout) reduction length.
     for (const auto& Ly : m->layers) {
         ld_qkv_ = std::max(ld_qkv_, Ly.rp[kQ] + Ly.rp[kK] + Ly.bt[kV].kp);

@@ -46,7 +46,7 @@ struct DeviceMatrix {
 // shared bases (family C) are uploaded once per storage instance.
 struct DeviceLayer {
     int r[kNumProj];
-    int rp[kNumProj];  // rank padded to 8: stride of the rank-space vectors
+    int rp[kNumProj];  // rank padded to 64: stride of the rank-space vectors
     DeviceMatrix at[kNumProj];
     DeviceMatrix bt[kNumProj];
     const float* attn_gamma;
