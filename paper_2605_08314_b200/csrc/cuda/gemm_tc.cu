@@ -17,6 +17,10 @@
 //               the fused epilogue straight from registers.
 // The dual (up/gate) GEMM runs the two K-loops into two TMEM accumulators and
 // applies silu(gate) * up in the epilogue, so up/gate never reach memory.
+// CG = 2 runs a CTA pair (tcgen05.mma.cta_group::2, M = 256 over two SMs, each
+// CTA holding half of the W tile); K splits of a tile can form one thread-block
+// cluster and reduce their fp32 partials through DSMEM before the epilogue
+// (A.cred), instead of a workspace round trip and splitk_reduce_kernel.
 #include <cuda.h>
 
 #include <algorithm>
