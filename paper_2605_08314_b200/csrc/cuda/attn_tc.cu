@@ -29,7 +29,7 @@ namespace fsvd::k {
 namespace {
 
 constexpr int kAQ = 128, kAK = 128;    // queries per CTA, keys per tile
-constexpr int kAThreads = 192;         // producer, MMA, 4 softmax warps
+constexpr int kAThreads = 320;         // producer, MMA, 8 softmax warps (two per TMEM lane group)
 constexpr int kBox = kAK * 128;        // one 64-dim x 128-row SW128 box: 16 KiB
 
 struct AttnTcArgs {
@@ -132,6 +132,7 @@ __global__ void __launch_bounds__(kAThreads, 1) attn_tc_kernel(const __grid_cons
     uint64_t *q_full = bars, *kv_full = bars + 1, *kv_empty = bars + 3, *s_full = bars + 5, *s_empty = bars + 7,
              *p_full = bars + 9, *o_full = bars + 10, *o_empty = bars + 11;
     uint32_t* tslot = reinterpret_cast<uint32_t*>(bars + 12);
+    float* xch = reinterpret_cast<float*>(bars + 16);  // [2 parities x 2 halves + 2 sums][128] row exchange
 
     asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
     asm volatile("griddepcontrol.wait;" ::: "memory");  // q, the cache rows and the length register
@@ -149,11 +150,11 @@ __global__ void __launch_bounds__(kAThreads, 1) attn_tc_kernel(const __grid_cons
             bar_init(&kv_full[i], 1);
             bar_init(&kv_empty[i], 1);
             bar_init(&s_full[i], 1);
-            bar_init(&s_empty[i], 128);
+            bar_init(&s_empty[i], 256);
         }
-        bar_init(p_full, 128);
+        bar_init(p_full, 256);
         bar_init(o_full, 1);
-        bar_init(o_empty, 128);
+        bar_init(o_empty, 256);
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
     if (warp == 1) {
@@ -214,39 +215,48 @@ __global__ void __launch_bounds__(kAThreads, 1) attn_tc_kernel(const __grid_cons
             }
         }
     } else {
-        // softmax: query row r = TMEM lane
+        // softmax: query row r = TMEM lane; two threads per row (warps 2-5 and 6-9 see
+        // the same TMEM lanes), half hf owns keys [64 hf, 64 hf + 64) of every tile
+        // and output columns [hf DH/2, hf DH/2 + DH/2); the row max is exchanged
+        // through shared memory, the row sums only at the end
+        constexpr int DH2 = DH / 2;
+        const int hf = (warp - 2) >> 2;
         const int r = (warp & 3) * 32 + lane;
         const int t = q0 + r, qpos = p0 + t;
         const uint32_t lane_base = tmem + (static_cast<uint32_t>((warp & 3) * 32) << 16);
         const float sl2 = a.scale * 1.4426950408889634f;  // scores in log2 units
-        float o[DH];
+        float o[DH2];
 #pragma unroll
-        for (int e = 0; e < DH; ++e) o[e] = 0.f;
+        for (int e = 0; e < DH2; ++e) o[e] = 0.f;
         float m = -CUDART_INF_F, l = 0.f, r_prev = 1.f;
-        uint8_t* prow = Ps + r * 128;
+        uint8_t* prow = Ps + hf * kBox + r * 128;  // this half's keys = P box hf
         for (int j = 0; j < ntiles; ++j) {
-            const int st = j & 1, k0 = j * kAK;
+            const int st = j & 1, k0 = j * kAK + hf * 64;
+            const uint32_t scol = lane_base + st * kAK + hf * 64;
             bar_wait(&s_full[st], (j >> 1) & 1);
             fence_after();
-            // pass 1: row max of the masked scores
+            // pass 1: row max of the masked scores (own 64 keys, then the other half's)
             float mx = -CUDART_INF_F;
 #pragma unroll 1
-            for (int c0 = 0; c0 < kAK; c0 += 32) {
+            for (int c0 = 0; c0 < 64; c0 += 32) {
                 float v[32];
-                tmem_ld32(lane_base + st * kAK + c0, v);
+                tmem_ld32(scol + c0, v);
 #pragma unroll
                 for (int i = 0; i < 32; ++i)
                     if (k0 + c0 + i <= qpos) mx = fmaxf(mx, v[i] * sl2);
             }
+            xch[((j & 1) * 2 + hf) * kAQ + r] = mx;
+            asm volatile("bar.sync 1, 256;" ::: "memory");
+            mx = fmaxf(mx, xch[((j & 1) * 2 + (hf ^ 1)) * kAQ + r]);
             const float mn = fmaxf(m, mx);
             // O (= the softmax-weighted sum through tile j-1) += O_{j-1}, rescaled
             if (j > 0) {
                 bar_wait(o_full, (j - 1) & 1);
                 fence_after();
 #pragma unroll
-                for (int c0 = 0; c0 < DH; c0 += 32) {
+                for (int c0 = 0; c0 < DH2; c0 += 32) {
                     float v[32];
-                    tmem_ld32(lane_base + kOcol + c0, v);
+                    tmem_ld32(lane_base + kOcol + hf * DH2 + c0, v);
 #pragma unroll
                     for (int i = 0; i < 32; ++i) o[c0 + i] = fmaf(o[c0 + i], r_prev, v[i]);
                 }
@@ -257,12 +267,12 @@ __global__ void __launch_bounds__(kAThreads, 1) attn_tc_kernel(const __grid_cons
             m = mn;
             l *= rs;
             r_prev = rs;
-            // pass 2: P = exp2(s - m) in bf16 into the K-major SW128 image (row r, keys
-            // [64 i, 64 i + 64) in box i, 16-B chunk c at c ^ (r & 7))
+            // pass 2: P = exp2(s - m) in bf16 into the K-major SW128 image (row r of
+            // box hf, 16-B chunk c at c ^ (r & 7))
 #pragma unroll 1
-            for (int c0 = 0; c0 < kAK; c0 += 32) {
+            for (int c0 = 0; c0 < 64; c0 += 32) {
                 float v[32];
-                tmem_ld32(lane_base + st * kAK + c0, v);
+                tmem_ld32(scol + c0, v);
                 uint32_t pk[16];
 #pragma unroll
                 for (int i = 0; i < 32; i += 2) {
@@ -271,27 +281,23 @@ __global__ void __launch_bounds__(kAThreads, 1) attn_tc_kernel(const __grid_cons
                     l += s0 + s1;
                     pk[i >> 1] = pack2(s0, s1);
                 }
-                uint8_t* box = prow + (c0 >> 6) * kBox;
 #pragma unroll
                 for (int u = 0; u < 4; ++u) {
-                    const int chunk = ((c0 & 63) >> 3) + u;
-                    *reinterpret_cast<uint4*>(box + ((chunk ^ (r & 7)) << 4)) =
+                    const int chunk = (c0 >> 3) + u;
+                    *reinterpret_cast<uint4*>(prow + ((chunk ^ (r & 7)) << 4)) =
                         make_uint4(pk[4 * u], pk[4 * u + 1], pk[4 * u + 2], pk[4 * u + 3]);
                 }
             }
             fence_before();
             bar_arrive(&s_empty[st]);
-            if (k0 + kAK > kend) {
+            if (j * kAK + kAK > kend && hf < NB) {
                 // last tile: V rows past the history are not this sequence's (stale or
-                // never written) -- zero them so 0 * garbage cannot reach O
-                const int key = k0 + r;
-                if (key >= kend) {
-                    uint8_t* vrow = Vs + st * kTile + r * 128;
+                // never written) -- zero them (box hf) so 0 * garbage cannot reach O
+                if (j * kAK + r >= kend) {
+                    uint8_t* vrow = Vs + st * kTile + hf * kBox + r * 128;
 #pragma unroll
-                    for (int i = 0; i < NB; ++i)
-#pragma unroll
-                        for (int c = 0; c < 8; ++c)
-                            *reinterpret_cast<uint4*>(vrow + i * kBox + c * 16) = make_uint4(0u, 0u, 0u, 0u);
+                    for (int c = 0; c < 8; ++c)
+                        *reinterpret_cast<uint4*>(vrow + c * 16) = make_uint4(0u, 0u, 0u, 0u);
                 }
             }
             asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // P / V stores -> the tensor core
@@ -300,18 +306,22 @@ __global__ void __launch_bounds__(kAThreads, 1) attn_tc_kernel(const __grid_cons
         bar_wait(o_full, (ntiles - 1) & 1);
         fence_after();
 #pragma unroll
-        for (int c0 = 0; c0 < DH; c0 += 32) {
+        for (int c0 = 0; c0 < DH2; c0 += 32) {
             float v[32];
-            tmem_ld32(lane_base + kOcol + c0, v);
+            tmem_ld32(lane_base + kOcol + hf * DH2 + c0, v);
 #pragma unroll
             for (int i = 0; i < 32; ++i) o[c0 + i] = fmaf(o[c0 + i], r_prev, v[i]);
         }
+        // row sum = both halves' partial sums (same running max)
+        xch[(4 + hf) * kAQ + r] = l;
+        asm volatile("bar.sync 1, 256;" ::: "memory");
+        l += xch[(4 + (hf ^ 1)) * kAQ + r];
         if (t < a.T) {
             const float inv = 1.f / l;
-            __nv_bfloat16* orow =
-                static_cast<__nv_bfloat16*>(a.out) + static_cast<long long>(b * a.T + t) * a.out_ld + h * DH;
+            __nv_bfloat16* orow = static_cast<__nv_bfloat16*>(a.out) + static_cast<long long>(b * a.T + t) * a.out_ld +
+                                  h * DH + hf * DH2;
 #pragma unroll
-            for (int e = 0; e < DH; e += 8)
+            for (int e = 0; e < DH2; e += 8)
                 *reinterpret_cast<uint4*>(orow + e) =
                     make_uint4(pack2(o[e] * inv, o[e + 1] * inv), pack2(o[e + 2] * inv, o[e + 3] * inv),
                                pack2(o[e + 4] * inv, o[e + 5] * inv), pack2(o[e + 6] * inv, o[e + 7] * inv));
@@ -365,7 +375,7 @@ bool attn_prefill_tcgen05(const AttnPrefillArgs& a, cudaStream_t s) {
     map2d(&A.kmap, a.kcache, a.d_head, kv_rows, a.d_head);
     map2d(&A.vmap, a.vcache, a.d_head, kv_rows, a.d_head);
     const int NB = a.d_head / 64;
-    const int smem = 5 * NB * kBox + 2 * kBox + 1024 + 256;  // Q, 2 x K, 2 x V, P, align, barriers
+    const int smem = 5 * NB * kBox + 2 * kBox + 1024 + 128 + 6 * 128 * 4;  // Q, 2 x K, 2 x V, P, align, barriers, row exchange
     dim3 grid((a.T + kAQ - 1) / kAQ, a.n_heads, a.batch);
     cudaLaunchConfig_t cfg{};
     cfg.gridDim = grid;
