@@ -37,8 +37,8 @@
 namespace fsvd::k {
 namespace mk {
 
-// full[stages], empty[stages], xbar -- rounded up to 128 B
-__host__ __device__ constexpr int mk_barrier_bytes(int stages) { return ((2 * stages + 1) * 8 + 127) / 128 * 128; }
+// full[stages], empty[stages], xbar, abar -- rounded up to 128 B
+__host__ __device__ constexpr int mk_barrier_bytes(int stages) { return ((2 * stages + 2) * 8 + 127) / 128 * 128; }
 
 // attention merge scratch: 3 x [pieces <= grid] floats in the record area
 constexpr int kMaxGrid = 256;
@@ -50,6 +50,7 @@ struct Smem {
     uint64_t* full;    // [stages]
     uint64_t* empty;   // [stages]
     uint64_t* xbar;
+    uint64_t* abar;    // attention pairs: the peer's merged half landed (rank 0 of a pair)
     void* x;           // staged input planes
     float* rec;        // [rec_chunks][16][B] / attention scratch
     float* misc;       // 256 floats
@@ -267,7 +268,15 @@ __device__ void gemv_phase(const MkGemv& g, const Smem& sm, GemvShared& sh, int 
         // follows (rows < pos are final; row pos is appended by this phase)
         const int H = g.seg[0].rows / g.d_head, len = sh.pos + 1;
         const RowSplit rs{B * H * len};
-        const int r0 = rs.lo(cta, G), r1 = rs.lo(cta + 1, G);
+        int r0 = rs.lo(cta, G), r1 = rs.lo(cta + 1, G);
+        if (g.attn_pairs) {  // this CTA's half of head cta / 2 (attn_pair_phase)
+            const int bh = cta >> 1, hf = cta & 1;
+            r0 = r1 = 0;
+            if (bh < B * H) {
+                r0 = bh * len + len * hf / 2;
+                r1 = bh * len + len * (hf + 1) / 2;
+            }
+        }
         for (int bh = r0 / len; r1 > r0 && bh <= (r1 - 1) / len; ++bh) {
             const int j0 = max(r0 - bh * len, 0), j1 = min(r1 - bh * len, len - 1);
             if (j1 <= j0) continue;
@@ -605,10 +614,17 @@ __device__ void attn_merge(const MkAttn& a, const Smem& sm, int tid, int cta, in
 // 16 at a time (all of a batch's K/V loads in flight), then the heads are
 // merged, the one shared with the next CTA first (publish, no wait).
 template <typename W, int B, int DH>
-__device__ void attn_phase(const MkAttn& a, const Smem& sm, int tid, int cta, int G, int pos) {
+__device__ void attn_pair_phase(const MkAttn& a, const Smem& sm, int tid, int cta, int pos, uint32_t aidx);
+
+template <typename W, int B, int DH>
+__device__ void attn_phase(const MkAttn& a, const Smem& sm, int tid, int cta, int G, int pos, uint32_t aidx) {
     constexpr int PER = DH / 32, KU = 16, ST = DH + 2;
     const int warp = tid >> 5, lane = tid & 31;
     const int len = pos + 1;
+    if (a.pairs) {
+        attn_pair_phase<W, B, DH>(a, sm, tid, cta, pos, aidx);
+        return;
+    }
     RowSplit rs{B * a.n_heads * len};
     const int r0 = rs.lo(cta, G), r1 = rs.lo(cta + 1, G);
     if (r1 <= r0) return;
@@ -702,6 +718,132 @@ __device__ void attn_phase(const MkAttn& a, const Smem& sm, int tid, int cta, in
     }
 }
 
+// One CTA pair (a thread-block cluster of 2 on one TPC) per (b, h): CTA half
+// hf attends keys [len hf / 2, len (hf + 1) / 2) with its 8 warps (16-key
+// batches, online softmax), merges its warps into one piece (acc, l, m), and
+// the second CTA stores its piece straight into the first one's shared memory
+// (st.shared::cluster + a release arrive per element on the first CTA's
+// mbarrier); the first CTA merges the two pieces and writes the o-projection
+// input. No global scratch, no cross-CTA polling.
+template <typename W, int B, int DH>
+__device__ void attn_pair_phase(const MkAttn& a, const Smem& sm, int tid, int cta, int pos, uint32_t aidx) {
+    constexpr int PER = DH / 32, KU = 16, ST = DH + 2;
+    const int warp = tid >> 5, lane = tid & 31;
+    const int len = pos + 1;
+    const int bh = cta >> 1, hf = cta & 1;
+    if (bh >= B * a.n_heads) return;
+    const int b = bh / a.n_heads, h = bh % a.n_heads;
+    const int lo = len * hf / 2, hi = len * (hf + 1) / 2;
+    const int n = hi - lo;
+    const int k0 = lo + n * warp / kConsumerWarps, k1 = lo + n * (warp + 1) / kConsumerWarps;
+    const W* Kc = static_cast<const W*>(a.kcache) + b * a.cache_bstride + h * a.cache_hstride;
+    const W* Vc = static_cast<const W*>(a.vcache) + b * a.cache_bstride + h * a.cache_hstride;
+    float qr[PER];
+    {
+        const float* q = a.qbuf + static_cast<size_t>(b) * a.q_ld + h * DH + lane * PER;
+#pragma unroll
+        for (int e = 0; e < PER; ++e) qr[e] = __ldcg(q + e) * a.scale;
+    }
+    float m = -CUDART_INF_F, l = 0.f, acc[PER];
+#pragma unroll
+    for (int e = 0; e < PER; ++e) acc[e] = 0.f;
+    using Raw = typename KvRaw<W, PER>::T;
+    for (int kb = k0; kb < k1; kb += KU) {
+        Raw kq[KU], vq[KU];
+#pragma unroll
+        for (int u = 0; u < KU; ++u) {
+            const int jj = min(kb + u, k1 - 1);  // clamp: duplicate loads are masked below
+            kq[u] = KvRaw<W, PER>::load(Kc + static_cast<long long>(jj) * DH + lane * PER);
+            vq[u] = KvRaw<W, PER>::load(Vc + static_cast<long long>(jj) * DH + lane * PER);
+        }
+        float sc[KU];
+        float mb = -CUDART_INF_F;
+#pragma unroll
+        for (int u = 0; u < KU; ++u) {
+            float kr[PER];
+            KvRaw<W, PER>::unpack(kq[u], kr);
+            float d = 0.f;
+#pragma unroll
+            for (int e = 0; e < PER; ++e) d = fmaf(qr[e], kr[e], d);
+            d = warp_sum(d);
+            sc[u] = kb + u < k1 ? d : -CUDART_INF_F;
+            mb = fmaxf(mb, sc[u]);
+        }
+        const float mn = fmaxf(m, mb);
+        const float r = expf(m - mn);  // exp(-inf) = 0 on the first round
+        l *= r;
+#pragma unroll
+        for (int e = 0; e < PER; ++e) acc[e] *= r;
+#pragma unroll
+        for (int u = 0; u < KU; ++u) {
+            float vr[PER];
+            KvRaw<W, PER>::unpack(vq[u], vr);
+            const float w = expf(sc[u] - mn);
+            l += w;
+#pragma unroll
+            for (int e = 0; e < PER; ++e) acc[e] = fmaf(w, vr[e], acc[e]);
+        }
+        m = mn;
+    }
+    float* wst = sm.rec;  // [warps][DH + 2]: acc, l, m
+#pragma unroll
+    for (int e = 0; e < PER; ++e) wst[warp * ST + lane * PER + e] = acc[e];
+    if (lane == 0) {
+        wst[warp * ST + DH] = l;
+        wst[warp * ST + DH + 1] = m;
+    }
+    consumer_sync();
+    // this CTA's piece: element e < DH (acc), DH (l); every thread computes the
+    // CTA max M itself (8 values)
+    float M = -CUDART_INF_F;
+    for (int w = 0; w < kConsumerWarps; ++w) M = fmaxf(M, wst[w * ST + DH + 1]);
+    auto piece = [&](int e) {
+        float t = 0.f;
+        for (int w = 0; w < kConsumerWarps; ++w) {
+            const float mw = wst[w * ST + DH + 1];
+            if (mw != -CUDART_INF_F) t += wst[w * ST + e] * expf(mw - M);
+        }
+        return t;
+    };
+    float* peer = sm.misc;  // [DH + 2] in the pair's first CTA: the second CTA's piece
+    if (hf == 1) {
+        if (tid < DH + 2) {
+            const float v = tid == DH + 1 ? M : piece(tid);
+            uint32_t ra, rb;
+            asm volatile("mapa.shared::cluster.u32 %0, %1, 0;"
+                         : "=r"(ra)
+                         : "r"(static_cast<uint32_t>(__cvta_generic_to_shared(peer + tid))));
+            asm volatile("mapa.shared::cluster.u32 %0, %1, 0;"
+                         : "=r"(rb)
+                         : "r"(static_cast<uint32_t>(__cvta_generic_to_shared(sm.abar))));
+            asm volatile("st.shared::cluster.f32 [%0], %1;" ::"r"(ra), "f"(v) : "memory");
+            asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(rb) : "memory");
+        }
+        consumer_sync();
+        return;
+    }
+    if (tid < DH) {
+        const float own = piece(tid), own_l = piece(DH);
+        {  // the peer's piece (acquire at cluster scope)
+            const uint32_t ba = static_cast<uint32_t>(__cvta_generic_to_shared(sm.abar));
+            asm volatile(
+                "{\n.reg .pred p;\nAW_%=:\n"
+                "mbarrier.try_wait.parity.acquire.cluster.shared::cta.b64 p, [%0], %1;\n"
+                "@!p bra AW_%=;\n}\n" ::"r"(ba),
+                "r"(aidx & 1u)
+                : "memory");
+        }
+        const float pm = *reinterpret_cast<volatile float*>(peer + DH + 1);
+        const float pl = *reinterpret_cast<volatile float*>(peer + DH);
+        const float pa = *reinterpret_cast<volatile float*>(peer + tid);
+        const float MM = fmaxf(M, pm);
+        const float so = M == -CUDART_INF_F ? 0.f : expf(M - MM), sp = pm == -CUDART_INF_F ? 0.f : expf(pm - MM);
+        const float L = own_l * so + pl * sp;
+        PlaneIO<W>::put(a.out, b, h * DH + tid, (own * so + pa * sp) / L);
+    }
+    consumer_sync();
+}
+
 // ------------------------------------------------------- argmax / vec ----
 template <int B>
 __device__ void argmax_phase(const MkArgmax& m, const Smem& sm, int tid, int cta) {
@@ -779,6 +921,7 @@ __global__ void __launch_bounds__(kThreads, 1) decode_mk_kernel(const __grid_con
     sm.full = reinterpret_cast<uint64_t*>(smem_raw + static_cast<size_t>(L.stages) * kChunkBytes);
     sm.empty = sm.full + L.stages;
     sm.xbar = sm.empty + L.stages;
+    sm.abar = sm.xbar + 1;
     sm.x = reinterpret_cast<char*>(sm.full) + mk_barrier_bytes(L.stages);
     sm.rec = reinterpret_cast<float*>(static_cast<char*>(sm.x) + L.x_bytes);
     const int rec_floats = std::max({L.rec_chunks * kTileRows * B, kConsumerWarps * (DH + 2), kAttnMergeFloats});
@@ -797,6 +940,7 @@ __global__ void __launch_bounds__(kThreads, 1) decode_mk_kernel(const __grid_con
             mbar_init(&sm.empty[i], 1);
         }
         mbar_init(sm.xbar, 1);
+        mbar_init(sm.abar, DH + 2);  // the peer's DH + 2 remote stores, one release arrive each
         mbar_init(&sm.dbar[0], 1);
         mbar_init(&sm.dbar[1], 1);
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
@@ -877,7 +1021,7 @@ __global__ void __launch_bounds__(kThreads, 1) decode_mk_kernel(const __grid_con
     }
     if (tid == 0) gsh.pos = L.pos ? __ldcg(L.pos) : 0;  // constant until the argmax phase (last of a step)
     consumer_sync();
-    uint32_t cseq = 0, xphase = 0;
+    uint32_t cseq = 0, xphase = 0, aidx = 0;
     const int nph = L.p_end - L.p_begin;
     // reps > 1: the phase program runs reps times back to back (reps decode steps
     // in one launch); gi counts phases over the whole launch
@@ -920,7 +1064,7 @@ __global__ void __launch_bounds__(kThreads, 1) decode_mk_kernel(const __grid_con
         const MkPhase& ph = sm.desc[buf];
         switch (ph.kind) {
             case kMkGemv: gemv_phase<W, B>(ph.g, sm, gsh, tid, cta, G, cseq, xphase, L.stages, tr, tr && cta == 0 ? L.trace + static_cast<size_t>(G) * nph * 16 : nullptr, sm.pstart[idx], sm.pstart[idx + 1], sm.ptiles[idx], L.progress ? L.progress + cta * 16 : nullptr); break;
-            case kMkAttn: attn_phase<W, B, DH>(ph.a, sm, tid, cta, G, gsh.pos); break;
+            case kMkAttn: attn_phase<W, B, DH>(ph.a, sm, tid, cta, G, gsh.pos, aidx++); break;
             case kMkArgmax: argmax_phase<B>(ph.m, sm, tid, cta); break;
             default: vec_phase<W, B>(ph.v, tid, cta, G); break;
         }
@@ -948,11 +1092,15 @@ void launch_t(const MkLaunch& L, cudaStream_t s) {
     cfg.blockDim = dim3(kThreads);
     cfg.dynamicSmemBytes = L.smem_bytes;
     cfg.stream = s;
-    cudaLaunchAttribute attr[1];
+    cudaLaunchAttribute attr[2];
     attr[0].id = cudaLaunchAttributeCooperative;
     attr[0].val.cooperative = 1;
+    attr[1].id = cudaLaunchAttributeClusterDimension;
+    attr[1].val.clusterDim.x = 2;
+    attr[1].val.clusterDim.y = 1;
+    attr[1].val.clusterDim.z = 1;
     cfg.attrs = attr;
-    cfg.numAttrs = 1;
+    cfg.numAttrs = L.cluster2 ? 2 : 1;
     cudaLaunchKernelEx(&cfg, fn, L);
 }
 

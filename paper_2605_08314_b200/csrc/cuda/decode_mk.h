@@ -66,6 +66,7 @@ struct MkGemv {
     long long cache_bstride, cache_hstride;
     int d_head;
     const int* pos;
+    int attn_pairs;   // the attention that follows runs one CTA pair per (b, h) (MkAttn::pairs)
     // kOutLogits
     float* logits;    // [B][vocab]
     int vocab;
@@ -91,6 +92,7 @@ struct MkAttn {
     int n_heads, d_head, splits;
     float scale;
     Planes out;          // merged output (o-projection input)
+    int pairs;           // 1: one CTA pair (a cluster of 2) per (b, h), halves merged through DSMEM
 };
 
 struct MkArgmax {
@@ -155,6 +157,7 @@ struct MkLaunch {
     int nphases;
     volatile int* progress; // optional host-mapped [grid][16] for hang diagnosis
     unsigned long long* trace;  // optional [grid][phases][4] %globaltimer stamps
+    int cluster2;               // launch as clusters of 2 CTAs (the attention pairs)
 };
 
 #ifndef FSVD_MK_CHUNK_LINES

@@ -810,6 +810,8 @@ void Session::init(const fsvd_session_opts& o) {
     mk_grid_ = std::min(mk_grid_, 256);
     if (const char* e = std::getenv("FSVD_MK_EXACT")) mk_exact_ = e[0] == '1';  // attention merge scratch is sized for <= 256 pieces per head
     mk_splits_ = mk_grid_;  // attention partial slots per head: one per contributing CTA
+    mk_attn_pairs_ = mk_grid_ % 2 == 0 && B_ * static_cast<int>(c.n_heads) <= mk_grid_ / 2;
+    if (const char* e = std::getenv("FSVD_MK_ATTN_PAIRS")) mk_attn_pairs_ = mk_attn_pairs_ && e[0] == '1';
     if (attn_route_ == FSVD_ATTN_LOWRANK_HISTORY) {
         for (const auto& Ly : m->layers) ld_hist_ = std::max({ld_hist_, Ly.r[kK], Ly.r[kV]});
         ld_hist_ = pad8(ld_hist_);
@@ -967,6 +969,7 @@ void Session::add_layer_phases(size_t l, const float* next_gamma) {
         g.cache_hstride = cache_hstride_;
         g.d_head = static_cast<int>(c.d_head);
         g.pos = pos_;
+        g.attn_pairs = mk_attn_pairs_ ? 1 : 0;
     }
     // dense-KV attention over cache rows [0, pos]
     {
@@ -987,6 +990,7 @@ void Session::add_layer_phases(size_t l, const float* next_gamma) {
         a.splits = mk_splits_;
         a.scale = static_cast<float>(1.0 / std::sqrt(static_cast<double>(c.d_head)));
         a.out = att_;
+        a.pairs = mk_attn_pairs_ ? 1 : 0;
         h_phases_.push_back(p);
     }
     // o projection, residual add (+ the FFN norm's gamma)
@@ -1147,6 +1151,7 @@ void Session::mk_run(int p_begin, int p_end, int reps) {
     L.x_bytes = x_bytes_;
     L.rec_chunks = rec_chunks_;
     L.l2_ahead = mk_l2_ahead_;
+    L.cluster2 = mk_attn_pairs_ ? 1 : 0;
     L.pos = pos_;
     L.chunks = d_chunks_;
     L.chunk_start = d_chunk_start_;

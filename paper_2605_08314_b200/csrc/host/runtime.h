@@ -204,6 +204,7 @@ class Session {
     volatile int* mk_progress_ = nullptr;
     int* mk_progress_host_ = nullptr;
     unsigned* mk_bar_ = nullptr;
+    bool mk_attn_pairs_ = false;  // decode attention: one CTA pair (cluster of 2) per (b, h) when B*H <= grid/2
     bool mk_exact_ = false;  // even unit splits for the kOutPlanes phases (FSVD_MK_EXACT=1; measured slower)
     int mk_smem_ = 0, mk_grid_ = 0, mk_splits_ = 0, mk_stages_ = 0, mk_l2_ahead_ = 16;
     int ph_head_ = 0, ph_argmax_ = 0, ph_pf_head_ = 0, ph_pf_argmax_ = 0;
