@@ -9,7 +9,8 @@ those paths with the CPU oracle:
   - a 512-token prefill, which uses the M = 512 tcgen05 GEMM tiles (256-row
     BMT = 2 tiles, split-K, 4-D weight tensor maps over the 11008-wide K);
   - >= 24 decode steps at context 512+, so each megakernel attention warp
-    runs several 16-key batches with the running-max rescale;
+    runs several 16-key batches with the running-max rescale, through both
+    attention splits (one CTA pair per head; the B*H*len row split);
   - the bench's 256-step multi-step launch (decode_steps), compared token by
     token and on the last logits.
 * C1 exactly (the `tiny` preset: d_head 64, 4 layers, prompt 32 + 32) in
@@ -55,8 +56,13 @@ def wide(fsvd, oracle_mod):
             "o32": o32, "pre32": pre32}
 
 
-def test_7b_width_prefill512_decode32(fsvd, oracle_mod, wide):
-    cfg = wide["cfg"]
+@pytest.mark.parametrize("attn", ["pairs", "rows"])
+def test_7b_width_prefill512_decode32(fsvd, oracle_mod, wide, attn, monkeypatch):
+    """attn = pairs: one CTA pair per head merged through DSMEM (the default at
+    B*H <= grid/2); rows: the B*H*len row split with per-head piece merges (the
+    path larger B*H takes), forced with FSVD_MK_ATTN_PAIRS=0."""
+    if attn == "rows":
+        monkeypatch.setenv("FSVD_MK_ATTN_PAIRS", "0")
     s = fsvd.Session(wide["model"], batch=1, capacity=1024, plan="full_step")
     assert s.engine()["megakernel"]
     lp = s.prefill(wide["prompt"][None])[0]
@@ -79,7 +85,7 @@ def test_7b_width_prefill512_decode32(fsvd, oracle_mod, wide):
         tok = int(np.argmax(want))
     assert max(errs) <= TOL["bf16"], errs
     assert s.position == 512 + 32
-    print(f"7B width: max rel err {max(errs):.3e}, greedy agreement {agree}/32")
+    print(f"7B width ({attn}): max rel err {max(errs):.3e}, greedy agreement {agree}/32")
 
 
 def test_7b_width_decode_steps_256(fsvd, oracle_mod, wide):
