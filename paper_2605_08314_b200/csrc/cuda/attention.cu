@@ -7,6 +7,7 @@
 #include <math_constants.h>
 
 #include <algorithm>
+#include <cstdlib>
 
 #include "common.cuh"
 #include "kernels.h"
@@ -374,6 +375,154 @@ __global__ void __launch_bounds__(kDThreads) attn_decode_kernel(const __grid_con
     if (threadIdx.x == 0) dst[DH + 1] = M;
 }
 
+// Same split-KV decode with the K / V rows of a split streamed into shared
+// memory by one producer thread (cp.async.bulk, 32 keys = 16 KiB per stage,
+// kBStages deep): the bytes in flight per SM no longer depend on registers.
+// Warp w reduces keys w, w + 4, ... of each stage (online softmax per warp, the
+// same order as attn_decode_kernel's per-warp batches is not required: the
+// warps are merged by max / rescale afterwards); same partial format.
+constexpr int kBKeys = 32, kBStages = 6, kBThreads = 160;  // 4 consumer warps + 1 producer warp
+
+__device__ __forceinline__ uint32_t sa32(const void* p) { return static_cast<uint32_t>(__cvta_generic_to_shared(p)); }
+
+template <int DH>
+__global__ void __launch_bounds__(kBThreads) attn_decode_bulk_kernel(const __grid_constant__ AttnPrefillArgs a,
+                                                                     float* part, int S) {
+    constexpr int PER = DH / 32, ST = DH + 2, NW = 4;
+    constexpr uint32_t kRow = DH * 2;  // bytes per key row (bf16)
+    extern __shared__ __align__(128) uint8_t bsm[];
+    uint8_t* ring = bsm;  // [stages][K 32 rows | V 32 rows]
+    uint64_t* full = reinterpret_cast<uint64_t*>(ring + kBStages * 2 * kBKeys * kRow);
+    uint64_t* empty = full + kBStages;
+    float* wst = reinterpret_cast<float*>(empty + kBStages);  // [NW][ST]
+    const int sp = blockIdx.x, h = blockIdx.y, b = blockIdx.z;
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    if (threadIdx.x == 0) {
+        for (int i = 0; i < kBStages; ++i) {
+            asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(sa32(&full[i])));
+            asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(sa32(&empty[i])), "r"(NW));
+        }
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    __syncthreads();
+    pdl_launch_dependents();
+    pdl_wait();
+    const int len = (a.p0_dev ? *a.p0_dev : a.p0) + 1;
+    const int j0 = static_cast<int>(static_cast<long long>(len) * sp / S);
+    const int j1 = static_cast<int>(static_cast<long long>(len) * (sp + 1) / S);
+    const int nchunks = (j1 - j0 + kBKeys - 1) / kBKeys;
+    const __nv_bfloat16* Kc = static_cast<const __nv_bfloat16*>(a.kcache) + b * a.cache_bstride + h * a.cache_hstride;
+    const __nv_bfloat16* Vc = static_cast<const __nv_bfloat16*>(a.vcache) + b * a.cache_bstride + h * a.cache_hstride;
+    auto wait = [&](uint64_t* bar, uint32_t par) {
+        asm volatile(
+            "{\n.reg .pred p;\nBW_%=:\nmbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n@!p bra BW_%=;\n}\n" ::"r"(
+                sa32(bar)),
+            "r"(par)
+            : "memory");
+    };
+    if (warp == NW) {
+        if (lane == 0) {
+            for (int c = 0; c < nchunks; ++c) {
+                const int st = c % kBStages;
+                const uint32_t par = (c / kBStages) & 1;
+                wait(&empty[st], par ^ 1);
+                const int k0 = j0 + c * kBKeys, n = min(kBKeys, j1 - k0);
+                const uint32_t bytes = static_cast<uint32_t>(n) * kRow;
+                uint8_t* dk = ring + st * 2 * kBKeys * kRow;
+                asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(sa32(&full[st])), "r"(2 * bytes)
+                             : "memory");
+                asm volatile(
+                    "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                        sa32(dk)),
+                    "l"(Kc + static_cast<long long>(k0) * DH), "r"(bytes), "r"(sa32(&full[st]))
+                    : "memory");
+                asm volatile(
+                    "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                        sa32(dk + kBKeys * kRow)),
+                    "l"(Vc + static_cast<long long>(k0) * DH), "r"(bytes), "r"(sa32(&full[st]))
+                    : "memory");
+            }
+        }
+        return;
+    }
+    float qr[PER];
+    {
+        const __nv_bfloat16* q = static_cast<const __nv_bfloat16*>(a.q) + static_cast<long long>(b) * a.q_ld + h * DH +
+                                 lane * PER;
+#pragma unroll
+        for (int e = 0; e < PER; ++e) qr[e] = __bfloat162float(q[e]) * a.scale;
+    }
+    float m = -CUDART_INF_F, l = 0.f, acc[PER];
+#pragma unroll
+    for (int e = 0; e < PER; ++e) acc[e] = 0.f;
+    constexpr int KW = kBKeys / NW;  // keys per warp per stage
+    for (int c = 0; c < nchunks; ++c) {
+        const int st = c % kBStages;
+        wait(&full[st], (c / kBStages) & 1);
+        const int n = min(kBKeys, j1 - (j0 + c * kBKeys));
+        const uint8_t* kb = ring + st * 2 * kBKeys * kRow;
+        const uint8_t* vb = kb + kBKeys * kRow;
+        uint2 kq[KW], vq[KW];
+#pragma unroll
+        for (int u = 0; u < KW; ++u) {
+            const int r = min(warp + NW * u, n - 1);  // clamp: masked below
+            kq[u] = *reinterpret_cast<const uint2*>(kb + r * kRow + lane * PER * 2);
+            vq[u] = *reinterpret_cast<const uint2*>(vb + r * kRow + lane * PER * 2);
+        }
+        __syncwarp();
+        if (lane == 0) asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(sa32(&empty[st])) : "memory");
+        float sc[KW];
+        float mb = -CUDART_INF_F;
+#pragma unroll
+        for (int u = 0; u < KW; ++u) {
+            float d = qr[0] * bf16lo(kq[u].x);
+            d = fmaf(qr[1], bf16hi(kq[u].x), d);
+            d = fmaf(qr[2], bf16lo(kq[u].y), d);
+            d = fmaf(qr[3], bf16hi(kq[u].y), d);
+            d = warp_sum(d);
+            sc[u] = warp + NW * u < n ? d : -CUDART_INF_F;
+            mb = fmaxf(mb, sc[u]);
+        }
+        const float mn = fmaxf(m, mb);
+        if (mn == -CUDART_INF_F) continue;
+        const float r = expf(m - mn);
+        l *= r;
+#pragma unroll
+        for (int e = 0; e < PER; ++e) acc[e] *= r;
+#pragma unroll
+        for (int u = 0; u < KW; ++u) {
+            const float w = expf(sc[u] - mn);
+            l += w;
+            acc[0] = fmaf(w, bf16lo(vq[u].x), acc[0]);
+            acc[1] = fmaf(w, bf16hi(vq[u].x), acc[1]);
+            acc[2] = fmaf(w, bf16lo(vq[u].y), acc[2]);
+            acc[3] = fmaf(w, bf16hi(vq[u].y), acc[3]);
+        }
+        m = mn;
+    }
+#pragma unroll
+    for (int e = 0; e < PER; ++e) wst[warp * ST + lane * PER + e] = acc[e];
+    if (lane == 0) {
+        wst[warp * ST + DH] = l;
+        wst[warp * ST + DH + 1] = m;
+    }
+    asm volatile("bar.sync 1, 128;" ::: "memory");
+    float M = -CUDART_INF_F;
+#pragma unroll
+    for (int w = 0; w < NW; ++w) M = fmaxf(M, wst[w * ST + DH + 1]);
+    float* dst = part + ((static_cast<long long>(b) * gridDim.y + h) * S + sp) * ST;
+    for (int e = threadIdx.x; e < DH + 1; e += NW * 32) {
+        float t = 0.f;
+#pragma unroll
+        for (int w = 0; w < NW; ++w) {
+            const float mw = wst[w * ST + DH + 1];
+            if (mw != -CUDART_INF_F) t += wst[w * ST + e] * expf(mw - M);
+        }
+        dst[e] = t;
+    }
+    if (threadIdx.x == 0) dst[DH + 1] = M;
+}
+
 template <int DH>
 __global__ void __launch_bounds__(DH) attn_decode_combine(const __grid_constant__ AttnPrefillArgs a, const float* part,
                                                           int S) {
@@ -398,15 +547,27 @@ __global__ void __launch_bounds__(DH) attn_decode_combine(const __grid_constant_
 }  // namespace
 
 int attn_decode_splits(int batch, int n_heads, int capacity) {
-    // >= 2 CTAs per SM over (B, H), each split >= 64 keys at full capacity
-    int S = (2 * 148 + batch * n_heads - 1) / (batch * n_heads);
+    // >= 1 CTA per SM over (B, H) (the bulk-copy kernel keeps ~96 KiB in flight per
+    // CTA; C3: 1 split 4.60 ms/step, 2: 4.70, 4: 4.74), each split >= 64 keys
+    int S = (148 + batch * n_heads - 1) / (batch * n_heads);
     S = std::min(S, std::max(1, capacity / 64));
+    if (const char* e = std::getenv("FSVD_ATTN_SPLITS")) S = std::atoi(e);  // development: forced split count
     return std::max(1, std::min(S, 64));
 }
 
 bool attn_decode(WType wt, const AttnPrefillArgs& a, float* part, int S, cudaStream_t s) {
     if (wt != kBF16 || a.T != 1 || a.d_head != 128 || a.q_ld % 4 || a.out_ld % 2) return false;
-    launch_pdl(attn_decode_kernel<128>, dim3(S, a.n_heads, a.batch), dim3(kDThreads), 0, s, a, part, S);
+    if (!std::getenv("FSVD_ATTN_DEC_REG")) {
+        constexpr int smem = kBStages * 2 * kBKeys * 256 + kBStages * 16 + 4 * (128 + 2) * 4;
+        static bool attr = false;
+        if (!attr) {
+            cudaFuncSetAttribute(attn_decode_bulk_kernel<128>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+            attr = true;
+        }
+        launch_pdl(attn_decode_bulk_kernel<128>, dim3(S, a.n_heads, a.batch), dim3(kBThreads), smem, s, a, part, S);
+    } else {
+        launch_pdl(attn_decode_kernel<128>, dim3(S, a.n_heads, a.batch), dim3(kDThreads), 0, s, a, part, S);
+    }
     launch_pdl(attn_decode_combine<128>, dim3(a.n_heads, a.batch), dim3(128), 0, s, a, static_cast<const float*>(part),
                S);
     return true;
