@@ -366,9 +366,10 @@ struct ChunkDot<__nv_bfloat16, B> {
         // fragments of the line's four k-steps are 32 contiguous bytes
         const __nv_bfloat16* xp = x + g * x_len + kbase + 16 * t;
         const uint32_t a_row = static_cast<uint32_t>(__cvta_generic_to_shared(buf)) + r * kLineBytes;
-        float d[4][4] = {};
-#pragma unroll 2
-        for (int l = 0; l < nl; ++l) {
+        // two accumulator sets (even / odd lines): the per-accumulator mma chain is
+        // half as long
+        float d[2][4][4] = {};
+        auto line = [&](int l, float (&dd)[4][4]) {
             const uint32_t lrow = a_row + l * kLineTileBytes;
             uint4 xb[2] = {make_uint4(0u, 0u, 0u, 0u), make_uint4(0u, 0u, 0u, 0u)};
             if (g < 2 * B) {
@@ -384,13 +385,27 @@ struct ChunkDot<__nv_bfloat16, B> {
                              : "r"(addr));
                 const uint4& q = xb[j >> 1];
                 const uint32_t b0 = (j & 1) ? q.z : q.x, b1 = (j & 1) ? q.w : q.y;
-                mma_bf16(d[j], a0, a1, a2, a3, b0, b1);
+                mma_bf16(dd[j], a0, a1, a2, a3, b0, b1);
             }
+        };
+        int l = 0;
+#pragma unroll 1
+        for (; l + 1 < nl; l += 2) {
+            line(l, d[0]);
+            line(l + 1, d[1]);
         }
+        if (l < nl) line(l, d[0]);
         if (t < B) {
-            rec[g * B + t] = ((d[0][0] + d[1][0]) + (d[2][0] + d[3][0])) + ((d[0][1] + d[1][1]) + (d[2][1] + d[3][1]));
-            rec[(g + 8) * B + t] =
-                ((d[0][2] + d[1][2]) + (d[2][2] + d[3][2])) + ((d[0][3] + d[1][3]) + (d[2][3] + d[3][3]));
+            float s0 = 0.f, s1 = 0.f;
+#pragma unroll
+            for (int p = 0; p < 2; ++p) {
+                s0 += ((d[p][0][0] + d[p][1][0]) + (d[p][2][0] + d[p][3][0])) +
+                      ((d[p][0][1] + d[p][1][1]) + (d[p][2][1] + d[p][3][1]));
+                s1 += ((d[p][0][2] + d[p][1][2]) + (d[p][2][2] + d[p][3][2])) +
+                      ((d[p][0][3] + d[p][1][3]) + (d[p][2][3] + d[p][3][3]));
+            }
+            rec[g * B + t] = s0;
+            rec[(g + 8) * B + t] = s1;
         }
     }
 };
