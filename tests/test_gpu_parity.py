@@ -118,9 +118,21 @@ def test_generate_matches_stepwise(fsvd, oracle_mod):
     assert s.position == 12 + 9
     om = oracle_mod.OracleModel.synthetic(spec)
     want = om.session(f64=True, capacity=512).generate(prompt[0], 10)
-    agree = float(np.mean(toks == want))
     assert toks[0] == want[0]  # first token always agrees in fp32 (margin >> 1e-4)
-    assert agree >= 0.5, (toks, want)
+    # exactness where it is decidable: teacher-forced with the GPU's own tokens, every
+    # greedy choice must equal the f64 oracle's whenever the oracle's top-2 margin
+    # exceeds the fp32 tolerance (2 x 1e-4 of the logit range)
+    o = om.session(f64=True, capacity=512)
+    lg = o.prefill(prompt[0])
+    decided = 0
+    for i in range(10):
+        top2 = np.sort(lg)[-2:]
+        if top2[1] - top2[0] > 2e-4 * np.max(np.abs(lg)):
+            assert toks[i] == int(np.argmax(lg)), (i, toks, want)
+            decided += 1
+        if i < 9:
+            lg = o.decode_step(int(toks[i]))
+    assert decided >= 8, decided
 
 
 def test_batch_sequences_independent(fsvd, oracle_mod):
