@@ -547,10 +547,21 @@ __global__ void __launch_bounds__(DH) attn_decode_combine(const __grid_constant_
 }  // namespace
 
 int attn_decode_splits(int batch, int n_heads, int capacity) {
-    // >= 1 CTA per SM over (B, H) (the bulk-copy kernel keeps ~96 KiB in flight per
-    // CTA; C3: 1 split 4.60 ms/step, 2: 4.70, 4: 4.74), each split >= 64 keys
-    int S = (148 + batch * n_heads - 1) / (batch * n_heads);
-    S = std::min(S, std::max(1, capacity / 64));
+    // Wave model of the bulk-copy kernel (2 CTAs per SM, ~96 KiB in flight each):
+    // time ~ waves x (4 us per CTA + keys per split x 21.5 ns), fitted to the C3 / C5
+    // split sweeps (C3 1 split 4.60 ms/step, 2: 4.70; C5 1: 6.40, 2: 6.50); a split
+    // must win by 5 %; splits keep >= 64 keys each.
+    const int n = batch * n_heads, slots = 2 * 148;
+    int S = 1;
+    double best = 1e30;
+    for (int sp = 1; sp <= 16 && capacity / sp >= 64; ++sp) {
+        const double waves = static_cast<double>((n * sp + slots - 1) / slots);
+        const double t = waves * (4.0 + 0.0215 * capacity / sp);
+        if (t < best * 0.95) {
+            best = t;
+            S = sp;
+        }
+    }
     if (const char* e = std::getenv("FSVD_ATTN_SPLITS")) S = std::atoi(e);  // development: forced split count
     return std::max(1, std::min(S, 64));
 }
