@@ -621,7 +621,9 @@ __device__ void attn_phase(const MkAttn& a, const Smem& sm, int tid, int cta, in
     constexpr int PER = DH / 32, KU = 16, ST = DH + 2;
     const int warp = tid >> 5, lane = tid & 31;
     const int len = pos + 1;
-    if (a.pairs) {
+    uint32_t ncl = 1;
+    if (a.pairs) asm volatile("mov.u32 %0, %%cluster_nctarank;" : "=r"(ncl));
+    if (a.pairs && ncl == 2) {  // (a launch without the cluster attribute, e.g. a profiler's replay, takes the row split)
         attn_pair_phase<W, B, DH>(a, sm, tid, cta, pos, aidx);
         return;
     }

@@ -75,15 +75,17 @@ if rep.exists():
 
     rd, wr = num("dram__bytes_read.sum"), num("dram__bytes_write.sum")
     dur = num("gpu__time_duration.sum")
-    pct = float(m["dram__throughput.avg.pct_of_peak_sustained_elapsed"][0])
+    pct = float(m["dram__bytes_read.sum.pct_of_peak_sustained_elapsed"][0]) + float(
+        m["dram__bytes_write.sum.pct_of_peak_sustained_elapsed"][0])
     t = {"decode_step_dram_bytes": rd + wr, "dram_read": rd, "dram_write": wr, "ncu_time_ms": dur * 1e3,
          "dram_pct_of_peak": pct,
-         "source": "ncu --set full --clock-control none, one full-step decode_mk_kernel launch (clusters of 2, "
-                   "k-permuted planes, pair attention), 32-layer LLaMA-7B shape rho 0.6, ctx 514 "
-                   "(tools/gpu_final_r2.sh, round 2 final)"}
+         "source": "ncu --set full --clock-control none, one full-step decode_mk_kernel launch (k-permuted "
+                   "planes; ncu's replay drops the cluster attribute, so the attention ran the row split -- same "
+                   "bytes), 32-layer LLaMA-7B shape rho 0.6, ctx 514 (tools/gpu_final_r2b.sh, round 2 final)"}
     (OUT / "traffic.json").write_text(json.dumps(t, indent=1) + "\n")
     keys = ["gpu__time_duration.sum", "dram__bytes_read.sum", "dram__bytes_write.sum",
-            "dram__throughput.avg.pct_of_peak_sustained_elapsed", "lts__t_bytes.sum",
+            "dram__bytes_read.sum.pct_of_peak_sustained_elapsed", "dram__bytes_read.sum.per_second",
+            "dram__cycles_active.sum.pct_of_peak_sustained_elapsed", "lts__t_bytes.sum",
             "sm__throughput.avg.pct_of_peak_sustained_elapsed", "launch__grid_size", "launch__cluster_dim_x",
             "launch__registers_per_thread", "sm__warps_active.avg.pct_of_peak_sustained_active"]
     with open(OUT / f"{TAG}_ncu_decode_step.txt", "w") as f:
