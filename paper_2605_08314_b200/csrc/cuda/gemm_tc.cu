@@ -340,14 +340,21 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_tc_kernel(const __grid_const
         } else {  // kGemmQKV: RoPE (interleaved pairs, math.hpp:30-44) + q store / KV append
             const int b = t / g.T, pos = (g.p0_dev ? *g.p0_dev : g.p0) + t % g.T;
             if (sg.epi != kEpiV) {
-                const float2* cs = g.rope + static_cast<long long>(pos) * (g.d_head / 2);
+                // the 32-column chunk lies inside one head (d_head is a multiple of 32): its 16
+                // (cos, sin) pairs are contiguous -- 8 vector loads, no per-pair index math
+                const float4* cs = reinterpret_cast<const float4*>(
+                    g.rope + static_cast<long long>(pos) * (g.d_head / 2) + ((n % g.d_head) >> 1));
 #pragma unroll
-                for (int i = 0; i < 32; i += 2) {
-                    const int ih = (n + i) % g.d_head;
-                    const float2 c = cs[ih >> 1];
-                    const float x0 = v[i], x1 = v[i + 1];
-                    v[i] = __fsub_rn(__fmul_rn(x0, c.x), __fmul_rn(x1, c.y));
-                    v[i + 1] = __fadd_rn(__fmul_rn(x0, c.y), __fmul_rn(x1, c.x));
+                for (int q = 0; q < 8; ++q) {
+                    const float4 c = __ldg(cs + q);
+#pragma unroll
+                    for (int u = 0; u < 2; ++u) {
+                        const int i = 4 * q + 2 * u;
+                        const float cx = u ? c.z : c.x, cy = u ? c.w : c.y;
+                        const float x0 = v[i], x1 = v[i + 1];
+                        v[i] = __fsub_rn(__fmul_rn(x0, cx), __fmul_rn(x1, cy));
+                        v[i + 1] = __fadd_rn(__fmul_rn(x0, cy), __fmul_rn(x1, cx));
+                    }
                 }
             }
             if (sg.epi == kEpiRopeQ) {
@@ -927,6 +934,7 @@ void launch(const TcArgs& ta, int tiles, int M, cudaStream_t s) {
 bool gemm_tc_supported(const GemmArgs& a) {
     // X row stride and segment offsets must allow 16 B-aligned TMA boxes
     if (a.x_ld % 8) return false;
+    if (a.epi == kGemmQKV && a.d_head % 32) return false;  // the RoPE epilogue's 32-column chunks stay in one head
     for (int i = 0; i < a.nseg; ++i)
         if (a.seg[i].x_off % 8) return false;
     return true;
