@@ -125,7 +125,8 @@ int main(int argc, char** argv) {
                 for (int sp = 1; sp <= spmax; ++sp) cfs.push_back({256, 2, sp, cg});
         }
         const size_t ybytes = size_t(M) * y_ld * (sh.epi == kGemmAddF32 ? 4 : 2);
-        std::vector<unsigned char> yref(ybytes), ygot(ybytes);
+        std::vector<unsigned char> yref(ybytes), ygot(ybytes), yprev(ybytes);
+        const Cf* prev = nullptr;
         for (const Cf& cf : cfs) {
             if (cf.cg == -1) setenv("FSVD_NO_CRED", "1", 1); else unsetenv("FSVD_NO_CRED");
             if (cf.cr) setenv("FSVD_GEMM_CRED", "1", 1); else unsetenv("FSVD_GEMM_CRED");
@@ -177,6 +178,16 @@ int main(int argc, char** argv) {
             float ms;
             cudaEventElapsedTime(&ms, e0, e1);
             cudaError_t err = cudaGetLastError();
+            // cluster twin of the previous config (same tile / splits, in-kernel DSMEM reduction instead of the
+            // reduction kernel): must be bitwise equal
+            const bool twin = prev && cf.bn != 0 && cf.sp != 0 &&
+                              ((mode == "cred" && prev->cg == -1 && cf.cg == 0 && prev->sp == cf.sp) ||
+                               (mode == "cred512" && prev->cr == 0 && cf.cr == 1 && prev->bn == cf.bn &&
+                                prev->sp == cf.sp && prev->cg == cf.cg));
+            if (twin) printf("PAIRCHECK %-5s M=%d BN=%d sp=%d CG=%d cluster vs reduction kernel: %s\n", sh.name, M, cf.bn,
+                             cf.sp, cf.cg, ygot == yprev ? "bitwise" : "DIFF");
+            yprev = cf.bn ? ygot : yref;
+            prev = &cf;
             const double fl = 2.0 * M * sh.k * (sh.epi == kGemmSilu ? 2.0 : 1.0) *
                               [&] { double n = 0; for (int r : sh.rows) n += r; return sh.epi == kGemmSilu ? n / 2 : n; }();
             printf("%-5s M=%d BN=%3d BMT=%d CG=%d sp=%d%s : %7.2f us %6.0f TF/s  %s maxdiff %.3g (max|y| %.3g) %s %s\n",
