@@ -225,6 +225,30 @@ __device__ __forceinline__ void store_bf16x32(__nv_bfloat16* dst, const float (&
     }
 }
 
+// RMSNorm fold: 1 / rms of row t from the per-32-column sums of squares of the
+// producing residual epilogue (GemmArgs::norm_ss_in), summed in index order
+__device__ __forceinline__ float norm_row_scale(const GemmArgs& g, int t) {
+    if (!g.norm_ss_in || t >= g.M) return 1.f;
+    const float4* p = reinterpret_cast<const float4*>(g.norm_ss_in + static_cast<long long>(t) * g.norm_ss_ld);
+    // 8 loads in flight per round, four partial sums, combined in a fixed order
+    float s0 = 0.f, s1 = 0.f, s2 = 0.f, s3 = 0.f;
+    const int n4 = g.norm_ss_n / 4;
+    for (int j = 0; j < n4; j += 8) {
+        float4 q[8];
+#pragma unroll
+        for (int u = 0; u < 8; ++u) q[u] = j + u < n4 ? __ldg(p + j + u) : make_float4(0.f, 0.f, 0.f, 0.f);
+#pragma unroll
+        for (int u = 0; u < 8; ++u) {
+            s0 += q[u].x;
+            s1 += q[u].y;
+            s2 += q[u].z;
+            s3 += q[u].w;
+        }
+    }
+    const float ss = (s0 + s1) + (s2 + s3);
+    return 1.0f / sqrtf(ss / static_cast<float>(g.norm_d) + g.norm_eps);
+}
+
 // -------------------------------------------------------------- kernel ----
 // BMT = 128-row M sub-tiles per CTA sharing each W tile (2: a 256 x BN tile in
 // two TMEM accumulators -- half the W traffic per FLOP of BMT = 1).
@@ -301,7 +325,7 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_tc_kernel(const __grid_const
     // K-loop of accumulator j: segment, x column offset, k-blocks
     auto seg_of = [&](int j) -> const GemvSeg& { return DUAL ? g.seg[j] : sg; };
     // fused epilogue of one 32-column chunk of output row t (columns n0 + c0 ..)
-    auto emit = [&](int t, int c0, float (&v)[32]) {
+    auto emit = [&](int t, int c0, float (&v)[32], float rs) {
         const int n = n0 + c0;
         const int valid = min(32, sg.rows - n);
         if (t >= g.M || valid <= 0) return;
@@ -320,6 +344,10 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_tc_kernel(const __grid_const
                     if (i < valid) w[i] = v[i];
             }
         } else if (g.epi == kGemmStore) {
+            if (g.norm_ss_in) {
+#pragma unroll
+                for (int i = 0; i < 32; ++i) v[i] *= rs;
+            }
             store_bf16x32(static_cast<__nv_bfloat16*>(g.y) + static_cast<long long>(t) * g.y_ld + sg.y_off + n, v,
                           valid);
         } else if (g.epi == kGemmAddF32) {
@@ -329,9 +357,31 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_tc_kernel(const __grid_const
 #pragma unroll
                 for (int i = 0; i < 8; ++i) r[i] = reinterpret_cast<const float4*>(y)[i];
 #pragma unroll
-                for (int i = 0; i < 8; ++i)
-                    reinterpret_cast<float4*>(y)[i] = make_float4(r[i].x + v[4 * i], r[i].y + v[4 * i + 1],
-                                                                  r[i].z + v[4 * i + 2], r[i].w + v[4 * i + 3]);
+                for (int i = 0; i < 8; ++i) {
+                    r[i] = make_float4(r[i].x + v[4 * i], r[i].y + v[4 * i + 1], r[i].z + v[4 * i + 2],
+                                       r[i].w + v[4 * i + 3]);
+                    reinterpret_cast<float4*>(y)[i] = r[i];
+                }
+                if (g.norm_xg) {  // the next RMSNorm's operands: x_new * gamma in bf16, sum of squares
+                    const float4* gm = reinterpret_cast<const float4*>(g.norm_gamma + sg.y_off + n);
+                    float ss = 0.f;
+#pragma unroll
+                    for (int i = 0; i < 8; ++i) {
+                        const float4 gv = __ldg(gm + i);
+                        ss = fmaf(r[i].x, r[i].x, ss);
+                        ss = fmaf(r[i].y, r[i].y, ss);
+                        ss = fmaf(r[i].z, r[i].z, ss);
+                        ss = fmaf(r[i].w, r[i].w, ss);
+                        v[4 * i] = r[i].x * gv.x;
+                        v[4 * i + 1] = r[i].y * gv.y;
+                        v[4 * i + 2] = r[i].z * gv.z;
+                        v[4 * i + 3] = r[i].w * gv.w;
+                    }
+                    store_bf16x32(static_cast<__nv_bfloat16*>(g.norm_xg) + static_cast<long long>(t) * g.norm_xg_ld +
+                                      sg.y_off + n,
+                                  v, 32);
+                    g.norm_ss[static_cast<long long>(t) * g.norm_ss_ld + (sg.y_off + n) / 32] = ss;
+                }
             } else {
 #pragma unroll
                 for (int i = 0; i < 32; ++i)
@@ -373,6 +423,7 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_tc_kernel(const __grid_const
     // Programmatic dependent launch: this grid may start while the previous
     // kernel drains. Only the weight tiles (constant) are read before
     // griddepcontrol.wait; activations are read and outputs written after it.
+    float rs_epi = 1.f;  // epilogue threads: the folded RMSNorm scale of their row (cluster path)
     asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
     if (warp == 0) {
         if (lane == 0) {
@@ -487,6 +538,9 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_tc_kernel(const __grid_const
         const int q = warp & 3;
         const int row = q * 32 + lane;
         asm volatile("griddepcontrol.wait;" ::: "memory");
+        // folded RMSNorm row scales, read while the mainloop runs
+        const float rs_mi[2] = {norm_row_scale(g, m0 + row), BMT > 1 ? norm_row_scale(g, m0 + BM * CG + row) : 1.f};
+        rs_epi = rs_mi[0];
         mbar_wait(tmem_full, 0);
         tc_fence_after();
         if (!DUAL && A.cred) {
@@ -503,7 +557,9 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_tc_kernel(const __grid_const
             }
         } else {
 #pragma unroll 1
-            for (int mi = 0; mi < BMT; ++mi)
+            for (int mi = 0; mi < BMT; ++mi) {
+                const int t = m0 + mi * BM * CG + row;
+                const float rs = rs_mi[mi];
 #pragma unroll 1
                 for (int c0 = 0; c0 < BN; c0 += 32) {
                     const uint32_t lane_addr = tmem_base + (static_cast<uint32_t>(q * 32) << 16) + mi * kAccStride;
@@ -514,8 +570,9 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_tc_kernel(const __grid_const
 #pragma unroll
                         for (int i = 0; i < 32; ++i) v[i] = silu_mul(gt[i], v[i]);
                     }
-                    emit(m0 + mi * BM * CG + row, c0, v);
+                    emit(t, c0, v, rs);
                 }
+            }
         }
     }
     tc_fence_before();
@@ -533,6 +590,7 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_tc_kernel(const __grid_const
             const int S = A.splits, cols = BN / S;
             const int z = static_cast<int>(blockIdx.z), row = (warp & 3) * 32 + lane;
             const uint32_t base = smem_u32(smem);
+            const float rs = rs_epi;  // (BMT = 1 in the cluster path)
 #pragma unroll 1
             for (int c0 = z * cols; c0 < (z + 1) * cols; c0 += 32) {
                 float v[32];
@@ -548,7 +606,7 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_tc_kernel(const __grid_const
                         v[i] = zz == 0 ? pv : v[i] + pv;
                     }
                 }
-                emit(m0 + row, c0, v);
+                emit(m0 + row, c0, v, rs);
             }
         }
         cluster_sync_all();  // peers have read this CTA's partial
@@ -869,6 +927,7 @@ __global__ void __launch_bounds__(256) splitk_reduce_kernel(const __grid_constan
     const GemmArgs& g = A.g;
     const size_t zs = static_cast<size_t>(g.M) * g.y_ld;  // partial stride
     const int t = blockIdx.y;
+    const float rs = norm_row_scale(g, t);
     for (int s = 0; s < g.nseg; ++s) {
         const GemvSeg& sg = g.seg[s];
         for (int n = blockIdx.x * 256 + threadIdx.x; n < sg.rows; n += gridDim.x * 256) {
@@ -886,7 +945,7 @@ __global__ void __launch_bounds__(256) splitk_reduce_kernel(const __grid_constan
             if (g.epi == kGemmAddF32)
                 static_cast<float*>(g.y)[c] += acc;
             else
-                static_cast<__nv_bfloat16*>(g.y)[c] = __float2bfloat16_rn(acc);
+                static_cast<__nv_bfloat16*>(g.y)[c] = __float2bfloat16_rn(g.norm_ss_in ? acc * rs : acc);
         }
     }
 }
@@ -1116,6 +1175,10 @@ void gemm_tc(const GemmArgs& a, int x_rows, cudaStream_t s) {
         std::sscanf(e, "%d,%d,%d,%d,%d", &x[0], &x[1], &x[2], &x[3], &x[4]);
         cred = x[4];
         if (cred && !dual) best_sp = std::max(1, x[2]);  // cluster splits need no workspace
+    }
+    if (a.norm_xg) {  // the residual epilogue emits the next RMSNorm's operands: one CTA per output chunk
+        best_sp = 1;
+        cred = 0;
     }
     if (cred && (dual || best_bmt != 1 || best_sp < 2 || (best_bn % (32 * best_sp)) != 0 || best_cg * best_sp > 8))
         cred = 0;

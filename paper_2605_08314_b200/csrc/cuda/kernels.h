@@ -87,6 +87,21 @@ struct GemmArgs {
     // tiles): fp32 [splits][M][y_ld]; null disables split-K
     float* ws;
     size_t ws_floats;
+    // RMSNorm folded into the GEMMs (tcgen05 path, prefill): a residual-add
+    // epilogue with norm_xg set also writes xg = bf16(x_new * norm_gamma)
+    // [M][norm_xg_ld] and the sums of squares of x_new per 32-column chunk into
+    // norm_ss [M][norm_ss_ld] (forces an unsplit launch); a plain-store epilogue
+    // with norm_ss_in set scales row t by 1 / sqrt(sum_j norm_ss_in[t][j] / norm_d
+    // + norm_eps), j < norm_ss_n (a multiple of 4) in index order, row stride
+    // norm_ss_ld -- x.A of the normalized row.
+    void* norm_xg;
+    int norm_xg_ld;
+    const float* norm_gamma;
+    float* norm_ss;
+    int norm_ss_ld;
+    const float* norm_ss_in;
+    int norm_ss_n, norm_d;
+    float norm_eps;
 };
 void gemm(WType wt, const GemmArgs& a, cudaStream_t s);       // dispatch: tcgen05 (bf16) / CUDA cores (f32)
 void gemm_simt(WType wt, const GemmArgs& a, cudaStream_t s);  // CUDA-core path

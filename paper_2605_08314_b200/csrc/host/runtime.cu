@@ -1321,8 +1321,9 @@ void Session::ensure_prefill_workspace(size_t rows) {
     pf_ws_floats_ = std::max(4ull * std::min<size_t>(rows, 1024), 64ull * std::min<size_t>(rows, 64)) *
                     std::max({ld_qkv_, ld_o_, ld_ug_, ld_d_, m.ldd});
     pf_ws_ = m.wt == k::kBF16 ? static_cast<float*>(dalloc(4 * pf_ws_floats_)) : nullptr;
+    pf_ss_ = static_cast<float*>(dalloc(rows * (m.ldd / 32) * 4));
     pf_rows_ = rows;
-    stats_.allocs += 11;
+    stats_.allocs += 12;
 }
 
 // One prefill chunk: tokens [b][t0 .. t0+Tc) of a [B][T_total] prompt.
@@ -1343,6 +1344,15 @@ void Session::layers_forward(int M, int Tc, int p0, const int* p0_dev) {
     const int d = static_cast<int>(c.d_model), ldd = m.ldd, ldff = m.ldff;
     const float eps = static_cast<float>(c.norm_eps);
     const size_t es = m.esize;
+    // RMSNorm folded into the GEMMs (prefill, tcgen05 path): the residual-add GEMMs
+    // (oB, downB) also emit x_new * gamma_next in bf16 and its per-32-column sums
+    // of squares; the next input-factor GEMM (upgateA, next layer's qkvA) reads
+    // those and scales its rows by 1 / rms -- no row-RMSNorm launch after layer 0
+    const bool fold = m.wt == k::kBF16 && M > 128 && !std::getenv("FSVD_PREFILL_SIMT") &&
+                      !std::getenv("FSVD_NO_NORM_FOLD") && d % 128 == 0 && ldd % 32 == 0;
+    const void* norm_ss_in = nullptr;  // set for the next plain-store GEMM that consumes a folded norm
+    void* norm_xg = nullptr;           // set for the next residual GEMM that emits one
+    const float* norm_gamma = nullptr;
     auto gemm = [&](const void* x, int x_ld, int nseg, std::initializer_list<k::GemvSeg> segs, int epi, void* y,
                     int y_ld, char* kc = nullptr, char* vc = nullptr) {
         k::GemmArgs g{};
@@ -1369,6 +1379,20 @@ void Session::layers_forward(int M, int Tc, int p0, const int* p0_dev) {
             g.ws = pf_ws_;
             g.ws_floats = pf_ws_floats_;
         }
+        if (epi == k::kGemmStore && norm_ss_in) {
+            g.norm_ss_in = static_cast<const float*>(norm_ss_in);
+            g.norm_ss_ld = ldd / 32;
+            g.norm_ss_n = d / 32;
+            g.norm_d = d;
+            g.norm_eps = eps;
+        }
+        if (epi == k::kGemmAddF32 && norm_xg) {
+            g.norm_xg = norm_xg;
+            g.norm_xg_ld = ldd;
+            g.norm_gamma = norm_gamma;
+            g.norm_ss = pf_ss_;
+            g.norm_ss_ld = ldd / 32;
+        }
         k::gemm(m.wt, g, stream_);
     };
     for (size_t l = 0; l < c.n_layers; ++l) {
@@ -1376,11 +1400,16 @@ void Session::layers_forward(int M, int Tc, int p0, const int* p0_dev) {
         char* kc = static_cast<char*>(kc_) + l * cache_lstride_ * es;
         char* vc = static_cast<char*>(vc_) + l * cache_lstride_ * es;
         const int rq = L.rp[kQ], rk = L.rp[kK];
-        k::rmsnorm_rows(m.wt, pf_x_, ldd, L.attn_gamma, eps, M, d, pf_xn_, ldd, stream_);
+        if (!fold || l == 0) {
+            k::rmsnorm_rows(m.wt, pf_x_, ldd, L.attn_gamma, eps, M, d, pf_xn_, ldd, stream_);
+        } else {
+            norm_ss_in = pf_ss_;  // pf_xn_ = x * attn_gamma from the previous layer's downB
+        }
         gemm(pf_xn_, ldd, 3,
              {seg(L.at[kQ], 0, 0, k::kEpiStore), seg(L.at[kK], 0, rq, k::kEpiStore),
               seg(L.at[kV], 0, rq + rk, k::kEpiStore)},
              k::kGemmStore, pf_pqkv_, ld_qkv_);
+        norm_ss_in = nullptr;
         if (attn_route_ == FSVD_ATTN_LOWRANK_HISTORY) {
             // record the pre-RoPE rank-space k / v rows of these positions
             const long long hstride = static_cast<long long>(cap_) * ld_hist_;
@@ -1451,13 +1480,22 @@ void Session::layers_forward(int M, int Tc, int p0, const int* p0_dev) {
                 k::attn_prefill(m.wt, a, stream_);
         }
         gemm(pf_att_, ldd, 1, {seg(L.at[kO], 0, 0, k::kEpiStore)}, k::kGemmStore, pf_po_, ld_o_);
+        if (fold) {
+            norm_xg = pf_xn_;
+            norm_gamma = L.mlp_gamma;
+        }
         gemm(pf_po_, ld_o_, 1, {seg(L.bt[kO], 0, 0, k::kEpiStore)}, k::kGemmAddF32, pf_x_, ldd);
+        norm_xg = nullptr;
         if (plan_ == FSVD_PLAN_SPLIT && Tc == 1) {  // split plan: attention | MLP boundary copy
             FSVD_CUDA(cudaMemcpyAsync(split_buf_, pf_x_, 4ull * M * ldd, cudaMemcpyDeviceToDevice, stream_));
             stats_.copy_bytes += 4ull * M * ldd;
             stats_.dispatches += 1;
         }
-        k::rmsnorm_rows(m.wt, pf_x_, ldd, L.mlp_gamma, eps, M, d, pf_xn_, ldd, stream_);
+        if (!fold) {
+            k::rmsnorm_rows(m.wt, pf_x_, ldd, L.mlp_gamma, eps, M, d, pf_xn_, ldd, stream_);
+        } else {
+            norm_ss_in = pf_ss_;  // pf_xn_ = x * mlp_gamma from oB
+        }
         if (ffn_ == FSVD_FFN_PACKED) {
             gemm(pf_xn_, ldd, 2, {seg(L.at[kUp], 0, 0, k::kEpiStore), seg(L.at[kGate], 0, L.rp[kUp], k::kEpiStore)},
                  k::kGemmStore, pf_pug_, ld_ug_);
@@ -1465,10 +1503,16 @@ void Session::layers_forward(int M, int Tc, int p0, const int* p0_dev) {
             gemm(pf_xn_, ldd, 1, {seg(L.at[kUp], 0, 0, k::kEpiStore)}, k::kGemmStore, pf_pug_, ld_ug_);
             gemm(pf_xn_, ldd, 1, {seg(L.at[kGate], 0, L.rp[kUp], k::kEpiStore)}, k::kGemmStore, pf_pug_, ld_ug_);
         }
+        norm_ss_in = nullptr;
         gemm(pf_pug_, ld_ug_, 2, {seg(L.bt[kUp], 0, 0, k::kEpiStore), seg(L.bt[kGate], L.rp[kUp], 0, k::kEpiStore)},
              k::kGemmSilu, pf_h_, ldff);
         gemm(pf_h_, ldff, 1, {seg(L.at[kDown], 0, 0, k::kEpiStore)}, k::kGemmStore, pf_pd_, ld_d_);
+        if (fold && l + 1 < c.n_layers) {
+            norm_xg = pf_xn_;
+            norm_gamma = m.layers[l + 1].attn_gamma;
+        }
         gemm(pf_pd_, ld_d_, 1, {seg(L.bt[kDown], 0, 0, k::kEpiStore)}, k::kGemmAddF32, pf_x_, ldd);
+        norm_xg = nullptr;
     }
 }
 

@@ -235,6 +235,7 @@ class Session {
     int32_t* pf_tok_ = nullptr;
     float* pf_ws_ = nullptr;
     size_t pf_ws_floats_ = 0;
+    float* pf_ss_ = nullptr;  // RMSNorm fold: sums of squares per 32-column chunk [rows][ldd / 32]
 };
 
 }  // namespace fsvd::rt
