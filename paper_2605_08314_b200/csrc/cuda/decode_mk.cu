@@ -1217,6 +1217,45 @@ int mk_max_stages(int x_bytes, int rec_chunks, int batch, int d_head, int nphase
 
 int mk_consumer_warps() { return mk::kConsumerWarps; }
 
+namespace {
+template <typename W, int B, int DH>
+int max_pairs_t(int smem_bytes) {
+    auto fn = mk::decode_mk_kernel<W, B, DH>;
+    cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, smem_bytes);
+    cudaLaunchConfig_t cfg{};
+    cfg.gridDim = dim3(2);
+    cfg.blockDim = dim3(mk::kThreads);
+    cfg.dynamicSmemBytes = smem_bytes;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeClusterDimension;
+    at[0].val.clusterDim.x = 2;
+    at[0].val.clusterDim.y = 1;
+    at[0].val.clusterDim.z = 1;
+    cfg.attrs = at;
+    cfg.numAttrs = 1;
+    int n = 0;
+    if (cudaOccupancyMaxActiveClusters(&n, fn, &cfg) != cudaSuccess) {
+        cudaGetLastError();
+        return 0;
+    }
+    return n;
+}
+}  // namespace
+
+int mk_max_active_pairs(WType wt, int batch, int d_head, int smem_bytes) {
+#define FSVD_MKP(W, BB, DHH) \
+    if (batch == BB && d_head == DHH) return max_pairs_t<W, BB, DHH>(smem_bytes);
+    if (wt == kBF16) {
+        FSVD_MKP(__nv_bfloat16, 1, 128) FSVD_MKP(__nv_bfloat16, 2, 128) FSVD_MKP(__nv_bfloat16, 1, 64)
+        FSVD_MKP(__nv_bfloat16, 2, 64) FSVD_MKP(__nv_bfloat16, 1, 32) FSVD_MKP(__nv_bfloat16, 2, 32)
+    } else {
+        FSVD_MKP(float, 1, 128) FSVD_MKP(float, 2, 128) FSVD_MKP(float, 1, 64) FSVD_MKP(float, 2, 64)
+        FSVD_MKP(float, 1, 32) FSVD_MKP(float, 2, 32)
+    }
+#undef FSVD_MKP
+    return 0;
+}
+
 bool mk_launch(WType wt, int batch, int d_head, const MkLaunch& L, cudaStream_t s) {
 #define FSVD_MK(W, BB, DHH) \
     if (batch == BB && d_head == DHH) { mk::launch_t<W, BB, DHH>(L, s); return true; }

@@ -184,6 +184,8 @@ int mk_smem_bytes(int stages, int x_bytes, int rec_chunks, int batch, int d_head
 int mk_max_stages(int x_bytes, int rec_chunks, int batch, int d_head, int nphases);
 int mk_consumer_warps();
 // false if (wt, batch, d_head) has no instantiation
+// co-resident 2-CTA clusters of the megakernel at the given shared memory (0 if unknown)
+int mk_max_active_pairs(WType wt, int batch, int d_head, int smem_bytes);
 bool mk_launch(WType wt, int batch, int d_head, const MkLaunch& L, cudaStream_t s);
 
 }  // namespace fsvd::k

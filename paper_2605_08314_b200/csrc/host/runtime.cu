@@ -811,6 +811,10 @@ void Session::init(const fsvd_session_opts& o) {
     if (const char* e = std::getenv("FSVD_MK_EXACT")) mk_exact_ = e[0] == '1';  // attention merge scratch is sized for <= 256 pieces per head
     mk_splits_ = mk_grid_;  // attention partial slots per head: one per contributing CTA
     mk_attn_pairs_ = mk_grid_ % 2 == 0 && B_ * static_cast<int>(c.n_heads) <= mk_grid_ / 2;
+    // the cooperative launch must fit as clusters of 2 (e.g. not under an SM-limited MPS share)
+    if (mk_attn_pairs_ && B_ <= 2 &&
+        2 * k::mk_max_active_pairs(m->wt, B_, static_cast<int>(c.d_head), 227 * 1024 - 1024) < mk_grid_)
+        mk_attn_pairs_ = false;
     if (const char* e = std::getenv("FSVD_MK_ATTN_PAIRS")) mk_attn_pairs_ = mk_attn_pairs_ && e[0] == '1';
     if (attn_route_ == FSVD_ATTN_LOWRANK_HISTORY) {
         for (const auto& Ly : m->layers) ld_hist_ = std::max({ld_hist_, Ly.r[kK], Ly.r[kV]});
