@@ -18,6 +18,7 @@
 #include <cuda.h>
 #include <math_constants.h>
 
+#include <cstdint>
 #include <cstdlib>
 #include <stdexcept>
 #include <string>
@@ -365,7 +366,8 @@ void map2d(CUtensorMap* m, const void* base, long long cols, long long rows, lon
 bool attn_prefill_tcgen05(const AttnPrefillArgs& a, cudaStream_t s) {
     if (std::getenv("FSVD_ATTN_MMA")) return false;
     if (a.d_head != 64 && a.d_head != 128) return false;
-    if (a.q_ld % 8 || a.cache_hstride % a.d_head || a.cache_bstride % a.d_head) return false;
+    if (a.q_ld % 8 || a.out_ld % 8 || a.cache_hstride % a.d_head || a.cache_bstride % a.d_head) return false;
+    if ((reinterpret_cast<uintptr_t>(a.q) | reinterpret_cast<uintptr_t>(a.out)) & 15) return false;
     AttnTcArgs A{};
     A.a = a;
     A.kv_row_b = a.cache_bstride / a.d_head;
