@@ -124,16 +124,19 @@ __global__ void __launch_bounds__(kAThreads, 1) attn_tc_kernel(const __grid_cons
     constexpr uint32_t kOcol = 256;             // TMEM: S buffers at columns 0 / 128, O_j at 256
     const AttnPrefillArgs& a = A.a;
     extern __shared__ __align__(1024) uint8_t sraw[];
-    uint8_t* sm = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(sraw) + 1023) & ~uintptr_t(1023));
+    // (no alignment slack: Q, 2 x K, 2 x V and 2 x P fill 224 KiB at d_head 128; the
+    // dynamic shared window starts on a 1 KiB boundary -- checked below)
+    uint8_t* sm = sraw;
     uint8_t* Qs = sm;
     uint8_t* Ks = Qs + kTile;           // [2] stages
     uint8_t* Vs = Ks + 2 * kTile;       // [2]
-    uint8_t* Ps = Vs + 2 * kTile;       // 128 queries x 128 keys bf16, K-major SW128 (2 boxes)
-    uint64_t* bars = reinterpret_cast<uint64_t*>(Ps + 2 * kBox);
+    uint8_t* Ps = Vs + 2 * kTile;       // [2] 128 queries x 128 keys bf16, K-major SW128 (2 boxes each)
+    uint64_t* bars = reinterpret_cast<uint64_t*>(Ps + 4 * kBox);
     uint64_t *q_full = bars, *kv_full = bars + 1, *kv_empty = bars + 3, *s_full = bars + 5, *s_empty = bars + 7,
-             *p_full = bars + 9, *o_full = bars + 10, *o_empty = bars + 11;
+             *p_full = bars + 9, *pv_done = bars + 10;  // pv_done[2]: P.V of the tiles using P buffer 0 / 1
     uint32_t* tslot = reinterpret_cast<uint32_t*>(bars + 12);
-    float* xch = reinterpret_cast<float*>(bars + 16);  // [2 parities x 2 halves + 2 sums][128] row exchange
+    float* xch = reinterpret_cast<float*>(bars + 16);  // [2 parities][2 halves][128] row exchange
+    if ((su32(sraw) & 1023u) != 0) __trap();
 
     asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
     asm volatile("griddepcontrol.wait;" ::: "memory");  // q, the cache rows and the length register
@@ -154,8 +157,8 @@ __global__ void __launch_bounds__(kAThreads, 1) attn_tc_kernel(const __grid_cons
             bar_init(&s_empty[i], 256);
         }
         bar_init(p_full, 256);
-        bar_init(o_full, 1);
-        bar_init(o_empty, 256);
+        bar_init(&pv_done[0], 1);
+        bar_init(&pv_done[1], 1);
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
     if (warp == 1) {
@@ -203,82 +206,102 @@ __global__ void __launch_bounds__(kAThreads, 1) attn_tc_kernel(const __grid_cons
             for (int j = 0; j < ntiles; ++j) {
                 const int st = j & 1;
                 if (j + 1 < ntiles) issue_s(j + 1);
-                bar_wait(p_full, j & 1);
-                bar_wait(o_empty, (j & 1) ^ 1);
+                bar_wait(p_full, j & 1);  // P_j written (and O rescaled, if the running max moved)
                 fence_after();
-                const uint32_t pa = su32(Ps), va = su32(Vs + st * kTile);
+                const uint32_t pa = su32(Ps + (j & 1) * 2 * kBox), va = su32(Vs + st * kTile);
 #pragma unroll
                 for (int kk = 0; kk < kAK / 16; ++kk)  // 16 keys per MMA: P +32 B, V +16 rows (2 KiB)
                     mma(tmem + kOcol, desc_k(pa + (kk >> 2) * kBox) + 2 * (kk & 3), desc_mn(va + kk * 2048), id_o,
-                        kk > 0);
-                commit(o_full);
+                        (j > 0 || kk > 0) ? 1u : 0u);  // O accumulates in TMEM over the key tiles
+                commit(&pv_done[j & 1]);
                 commit(&kv_empty[st]);
             }
         }
     } else {
         // softmax: query row r = TMEM lane; two threads per row (warps 2-5 and 6-9 see
-        // the same TMEM lanes), half hf owns keys [64 hf, 64 hf + 64) of every tile
-        // and output columns [hf DH/2, hf DH/2 + DH/2); the row max is exchanged
-        // through shared memory, the row sums only at the end
+        // the same TMEM lanes), half hf owns keys [64 hf, 64 hf + 64) of every tile and
+        // output columns [hf DH/2, hf DH/2 + DH/2). Each S row is read from TMEM once
+        // (into registers); O accumulates in TMEM (P.V with accumulate) and is rescaled
+        // there only when the running max grows by more than kTau (log2 units) -- exact,
+        // since P and the row sum use the same reference max. P is double-buffered, so
+        // writing P_j waits for P.V of tile j - 2, not j - 1. The row max is exchanged
+        // through shared memory, the row sums only at the end.
         constexpr int DH2 = DH / 2;
+        constexpr float kTau = 8.0f;
         const int hf = (warp - 2) >> 2;
         const int r = (warp & 3) * 32 + lane;
         const int t = q0 + r, qpos = p0 + t;
         const uint32_t lane_base = tmem + (static_cast<uint32_t>((warp & 3) * 32) << 16);
+        const uint32_t ocol = lane_base + kOcol + hf * DH2;
         const float sl2 = a.scale * 1.4426950408889634f;  // scores in log2 units
-        float o[DH2];
-#pragma unroll
-        for (int e = 0; e < DH2; ++e) o[e] = 0.f;
-        float m = -CUDART_INF_F, l = 0.f, r_prev = 1.f;
-        uint8_t* prow = Ps + hf * kBox + r * 128;  // this half's keys = P box hf
+        float m = -CUDART_INF_F, l = 0.f;
+        // P.V of tile i has completed: completion (i >> 1) of pv_done[i & 1] (parity (i >> 1) & 1)
+        auto wait_pv = [&](int i) { bar_wait(&pv_done[i & 1], (i >> 1) & 1); };
         for (int j = 0; j < ntiles; ++j) {
             const int st = j & 1, k0 = j * kAK + hf * 64;
             const uint32_t scol = lane_base + st * kAK + hf * 64;
+            uint8_t* prow = Ps + (j & 1) * 2 * kBox + hf * kBox + r * 128;  // P buffer j & 1, box hf
             bar_wait(&s_full[st], (j >> 1) & 1);
             fence_after();
-            // pass 1: row max of the masked scores (own 64 keys, then the other half's)
-            float mx = -CUDART_INF_F;
-#pragma unroll 1
-            for (int c0 = 0; c0 < 64; c0 += 32) {
+            float sv[64];
+            {
                 float v[32];
-                tmem_ld32(scol + c0, v);
+                tmem_ld32(scol, v);
 #pragma unroll
-                for (int i = 0; i < 32; ++i)
-                    if (k0 + c0 + i <= qpos) mx = fmaxf(mx, v[i] * sl2);
+                for (int i = 0; i < 32; ++i) sv[i] = v[i];
+                tmem_ld32(scol + 32, v);
+#pragma unroll
+                for (int i = 0; i < 32; ++i) sv[32 + i] = v[i];
+            }
+            fence_before();
+            bar_arrive(&s_empty[st]);  // the S buffer is free for tile j + 2
+            float mx = -CUDART_INF_F;
+#pragma unroll
+            for (int i = 0; i < 64; ++i) {
+                sv[i] = k0 + i <= qpos ? sv[i] * sl2 : -CUDART_INF_F;
+                mx = fmaxf(mx, sv[i]);
             }
             xch[((j & 1) * 2 + hf) * kAQ + r] = mx;
             asm volatile("bar.sync 1, 256;" ::: "memory");
             mx = fmaxf(mx, xch[((j & 1) * 2 + (hf ^ 1)) * kAQ + r]);
-            const float mn = fmaxf(m, mx);
-            // O (= the softmax-weighted sum through tile j-1) += O_{j-1}, rescaled
-            if (j > 0) {
-                bar_wait(o_full, (j - 1) & 1);
-                fence_after();
+            if (mx != -CUDART_INF_F && (m == -CUDART_INF_F || mx > m + kTau)) {
+                const float f = m == -CUDART_INF_F ? 0.f : exp2f(m - mx);
+                if (j > 0 && m != -CUDART_INF_F) {  // O *= f in TMEM once P.V of tile j - 1 is done (rare)
+                    wait_pv(j - 1);
+                    fence_after();
 #pragma unroll
-                for (int c0 = 0; c0 < DH2; c0 += 32) {
-                    float v[32];
-                    tmem_ld32(lane_base + kOcol + hf * DH2 + c0, v);
+                    for (int c0 = 0; c0 < DH2; c0 += 32) {
+                        float v[32];
+                        tmem_ld32(ocol + c0, v);
+                        uint32_t w[32];
 #pragma unroll
-                    for (int i = 0; i < 32; ++i) o[c0 + i] = fmaf(o[c0 + i], r_prev, v[i]);
+                        for (int i = 0; i < 32; ++i) w[i] = __float_as_uint(v[i] * f);
+                        asm volatile(
+                            "tcgen05.st.sync.aligned.32x32b.x32.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,"
+                            "%14,%15,%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31,%32};" ::"r"(
+                                ocol + c0),
+                            "r"(w[0]), "r"(w[1]), "r"(w[2]), "r"(w[3]), "r"(w[4]), "r"(w[5]), "r"(w[6]), "r"(w[7]),
+                            "r"(w[8]), "r"(w[9]), "r"(w[10]), "r"(w[11]), "r"(w[12]), "r"(w[13]), "r"(w[14]),
+                            "r"(w[15]), "r"(w[16]), "r"(w[17]), "r"(w[18]), "r"(w[19]), "r"(w[20]), "r"(w[21]),
+                            "r"(w[22]), "r"(w[23]), "r"(w[24]), "r"(w[25]), "r"(w[26]), "r"(w[27]), "r"(w[28]),
+                            "r"(w[29]), "r"(w[30]), "r"(w[31])
+                            : "memory");
+                    }
+                    asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
                 }
-                fence_before();
-                bar_arrive(o_empty);
+                l *= f;
+                m = mx;
             }
-            const float rs = mn == -CUDART_INF_F ? 1.f : exp2f(m - mn);  // exp2(-inf) = 0 on the first tile
-            m = mn;
-            l *= rs;
-            r_prev = rs;
-            // pass 2: P = exp2(s - m) in bf16 into the K-major SW128 image (row r of
-            // box hf, 16-B chunk c at c ^ (r & 7))
-#pragma unroll 1
+            if (j >= 2) wait_pv(j - 2);  // P buffer j & 1 was read by P.V of tile j - 2
+            // P = exp2(s - m) in bf16 into the K-major SW128 image (row r of box hf,
+            // 16-B chunk c at c ^ (r & 7))
+#pragma unroll
             for (int c0 = 0; c0 < 64; c0 += 32) {
-                float v[32];
-                tmem_ld32(scol + c0, v);
                 uint32_t pk[16];
 #pragma unroll
                 for (int i = 0; i < 32; i += 2) {
-                    const float s0 = k0 + c0 + i <= qpos && mn != -CUDART_INF_F ? exp2f(v[i] * sl2 - mn) : 0.f;
-                    const float s1 = k0 + c0 + i + 1 <= qpos && mn != -CUDART_INF_F ? exp2f(v[i + 1] * sl2 - mn) : 0.f;
+                    const float s0 = m == -CUDART_INF_F ? 0.f : exp2f(sv[c0 + i] - m);
+                    const float s1 = m == -CUDART_INF_F ? 0.f : exp2f(sv[c0 + i + 1] - m);
                     l += s0 + s1;
                     pk[i >> 1] = pack2(s0, s1);
                 }
@@ -289,8 +312,6 @@ __global__ void __launch_bounds__(kAThreads, 1) attn_tc_kernel(const __grid_cons
                         make_uint4(pk[4 * u], pk[4 * u + 1], pk[4 * u + 2], pk[4 * u + 3]);
                 }
             }
-            fence_before();
-            bar_arrive(&s_empty[st]);
             if (j * kAK + kAK > kend && hf < NB) {
                 // last tile: V rows past the history are not this sequence's (stale or
                 // never written) -- zero them (box hf) so 0 * garbage cannot reach O
@@ -301,31 +322,31 @@ __global__ void __launch_bounds__(kAThreads, 1) attn_tc_kernel(const __grid_cons
                         *reinterpret_cast<uint4*>(vrow + c * 16) = make_uint4(0u, 0u, 0u, 0u);
                 }
             }
+            fence_before();
             asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // P / V stores -> the tensor core
             bar_arrive(p_full);
         }
-        bar_wait(o_full, (ntiles - 1) & 1);
+        wait_pv(ntiles - 1);
         fence_after();
+        // row sum = both halves' partial sums (same reference max); the exchange slot of
+        // parity ntiles & 1 was last read before the final iteration's barrier
+        xch[((ntiles & 1) * 2 + hf) * kAQ + r] = l;
+        asm volatile("bar.sync 1, 256;" ::: "memory");
+        l += xch[((ntiles & 1) * 2 + (hf ^ 1)) * kAQ + r];
+        const float inv = 1.f / l;
+        __nv_bfloat16* orow = static_cast<__nv_bfloat16*>(a.out) + static_cast<long long>(b * a.T + t) * a.out_ld +
+                              h * DH + hf * DH2;
 #pragma unroll
         for (int c0 = 0; c0 < DH2; c0 += 32) {
             float v[32];
-            tmem_ld32(lane_base + kOcol + hf * DH2 + c0, v);
+            tmem_ld32(ocol + c0, v);  // (all lanes: .sync.aligned)
+            if (t < a.T) {
 #pragma unroll
-            for (int i = 0; i < 32; ++i) o[c0 + i] = fmaf(o[c0 + i], r_prev, v[i]);
-        }
-        // row sum = both halves' partial sums (same running max)
-        xch[(4 + hf) * kAQ + r] = l;
-        asm volatile("bar.sync 1, 256;" ::: "memory");
-        l += xch[(4 + (hf ^ 1)) * kAQ + r];
-        if (t < a.T) {
-            const float inv = 1.f / l;
-            __nv_bfloat16* orow = static_cast<__nv_bfloat16*>(a.out) + static_cast<long long>(b * a.T + t) * a.out_ld +
-                                  h * DH + hf * DH2;
-#pragma unroll
-            for (int e = 0; e < DH2; e += 8)
-                *reinterpret_cast<uint4*>(orow + e) =
-                    make_uint4(pack2(o[e] * inv, o[e + 1] * inv), pack2(o[e + 2] * inv, o[e + 3] * inv),
-                               pack2(o[e + 4] * inv, o[e + 5] * inv), pack2(o[e + 6] * inv, o[e + 7] * inv));
+                for (int e = 0; e < 32; e += 8)
+                    *reinterpret_cast<uint4*>(orow + c0 + e) =
+                        make_uint4(pack2(v[e] * inv, v[e + 1] * inv), pack2(v[e + 2] * inv, v[e + 3] * inv),
+                                   pack2(v[e + 4] * inv, v[e + 5] * inv), pack2(v[e + 6] * inv, v[e + 7] * inv));
+            }
         }
     }
     fence_before();
@@ -377,7 +398,7 @@ bool attn_prefill_tcgen05(const AttnPrefillArgs& a, cudaStream_t s) {
     map2d(&A.kmap, a.kcache, a.d_head, kv_rows, a.d_head);
     map2d(&A.vmap, a.vcache, a.d_head, kv_rows, a.d_head);
     const int NB = a.d_head / 64;
-    const int smem = 5 * NB * kBox + 2 * kBox + 1024 + 128 + 6 * 128 * 4;  // Q, 2 x K, 2 x V, P, align, barriers, row exchange
+    const int smem = 5 * NB * kBox + 4 * kBox + 128 + 4 * 128 * 4;  // Q, 2 x K, 2 x V, 2 x P, barriers, row exchange
     dim3 grid((a.T + kAQ - 1) / kAQ, a.n_heads, a.batch);
     cudaLaunchConfig_t cfg{};
     cfg.gridDim = grid;
